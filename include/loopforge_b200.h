@@ -1,0 +1,131 @@
+/*
+ * loopforge_b200.h -- C ABI of the B200 executor for Fortran-ingested,
+ * transformed loopforge kernels.
+ *
+ * The reference has no plugin/operator registry; its two
+ * execution boundaries are
+ *   (1) interpret(kernel, env) -> env
+ *       /root/reference/pkg/src/loopforge/interp.py:323-400, and
+ *   (2) the C function emitted by emit(kernel, "c") and called by the test
+ *       harness  /root/reference/pkg/src/loopforge/codegen.py:511-527
+ *       (signature) and /root/reference/pkg/tests/c_oracle.py:59-74 (call).
+ * Each entry point below replaces one emitted function: the leading
+ * arguments are exactly the emitted-C parameters (kernel.args in declaration
+ * order -- arrays as pointers, const iff not an output, scalars by value --
+ * then the remaining integer parameters sorted by name, codegen.py:511-527),
+ * except that pointers are DEVICE pointers.  Two arguments are appended: the
+ * logical launch geometry derived from the kernel's g.N/l.N tags and the
+ * CUDA stream to launch on.
+ *
+ * Conventions
+ *   - Every entry returns LFB_OK (0) or an LFB_ERR_* code; the text of the
+ *     last error on the calling thread is available from lfb_last_error().
+ *     LFB_ERR_UNSUPPORTED maps to loopforge.errors.CodegenError
+ *     (codegen.py:470-472, 574-577), LFB_ERR_LAUNCH / LFB_ERR_ARG to
+ *     InterpError (interp.py:103-112).
+ *   - Launches are asynchronous and stream ordered; nothing synchronises.
+ *   - The caller owns all device memory; no entry allocates or frees caller
+ *     buffers.  Scratch (the SEM norm partials) is caller provided.
+ *   - Index arithmetic inside kernels is 64-bit (the emitted C uses int and
+ *     overflows past 2^31 elements, SURVEY.md §7 hard part 2).
+ *   - Results are bitwise identical to the reference's execution of the same
+ *     kernel (fill, axpy, matvec, semlap); sgemm is within the fp32 tolerance
+ *     documented in DESIGN.md.
+ */
+#ifndef LOOPFORGE_B200_H
+#define LOOPFORGE_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LFB_ABI_VERSION 1
+
+enum {
+    LFB_OK = 0,
+    LFB_ERR_UNSUPPORTED = 1, /* -> CodegenError */
+    LFB_ERR_LAUNCH = 2,      /* -> InterpError  */
+    LFB_ERR_ARG = 3          /* -> InterpError  */
+};
+
+/* cudaStream_t without pulling in the CUDA headers. */
+typedef struct CUstream_st *lfb_stream;
+
+/* Logical launch geometry (paper_1503_07659_b200/launch.py), i.e. what the
+ * reference's OpenCL prologue would index with get_group_id/get_local_id
+ * (codegen.py:580-612).  A NULL geometry means "untransformed kernel": the
+ * executor picks its own decomposition. */
+typedef struct lfb_launch {
+    int32_t abi_version;      /* must be LFB_ABI_VERSION                    */
+    int32_t guard;            /* 1 iff the reference emits an OpenCL guard   */
+    int64_t group_extent[3];  /* extents of the g.0..g.2 inames; 0 in
+                                 group_extent[0] = no parallel tags
+                                 (untransformed kernel): the executor
+                                 chooses the decomposition               */
+    int32_t local_extent[3];  /* extents of the l.0..l.2 inames              */
+    int32_t npts;             /* semlap: points per direction (order + 1)    */
+    int32_t sm_count;         /* 0: query the device                         */
+    int32_t ctas_per_sm;      /* 0: kernel default                           */
+    int32_t variant;          /* 0: default kernel variant                   */
+    int32_t reserved;
+    double *sumsq;            /* semlap: if non-NULL receives sum(w*w)       */
+    double *workspace;        /* semlap: >= lfb_semlap_workspace() doubles   */
+    int64_t workspace_len;
+} lfb_launch;
+
+int lfb_abi_version(void);
+const char *lfb_last_error(void);
+/* SMs of the current device (148 on B200), or -1. */
+int lfb_device_sm_count(void);
+
+/* fill: out[i] = a                      emitted: void fill(double *out, double a, int n)
+ * reference: tests/test_fortran.py:13-27, tests/test_codegen.py:217-234   */
+int lfb_fill_f64(double *out, double a, int n,
+                 const lfb_launch *geom, lfb_stream stream);
+int lfb_fill_f32(float *out, float a, int n,
+                 const lfb_launch *geom, lfb_stream stream);
+
+/* axpy: y[i] = y[i] + alpha*x[i]        emitted: void axpy(double *y, double const *x, double alpha, int n)
+ * reference: SURVEY.md Appendix B                                         */
+int lfb_axpy_f64(double *y, const double *x, double alpha, int n,
+                 const lfb_launch *geom, lfb_stream stream);
+int lfb_axpy_f32(float *y, const float *x, float alpha, int n,
+                 const lfb_launch *geom, lfb_stream stream);
+
+/* matvec: y[i] = sum_j a[i + n*j]*x[j], sequential j, s starts at 0
+ *                                       emitted: void matvec(double *y, double const *a, double const *x, int n)
+ * reference: SURVEY.md Appendix B (extract_subst + precompute on x)       */
+int lfb_matvec_f64(double *y, const double *a, const double *x, int n,
+                   const lfb_launch *geom, lfb_stream stream);
+
+/* semlap: tensor-product SEM Laplacian, geom->npts points per direction
+ *                                       emitted: void semlap(double *w, double const *u, double const *d, double const *g, int nelt)
+ * reference: SURVEY.md Appendix A; layouts u,w (n,n,n,nelt) strides
+ * (1,n,n^2,n^3), d (n,n) strides (1,n), g (6,n,n,n,nelt) strides
+ * (1,6,6n,6n^2,6n^3) -- fortran.py:638-658 column-major lowering.        */
+int lfb_semlap_f64(double *w, const double *u, const double *d,
+                   const double *g, int nelt,
+                   const lfb_launch *geom, lfb_stream stream);
+/* doubles of workspace lfb_semlap_f64 needs when geom->sumsq != NULL */
+int64_t lfb_semlap_workspace(int npts, int nelt, const lfb_launch *geom);
+
+/* sgemm: c[i,j] = c[i,j] + alpha*b[k,j]*a[i,k] over ascending k, all
+ * column major: a (m,l), b (l,n), c (m,n)
+ *                                       emitted: void sgemm(float alpha, float const *a, float const *b, float *c, int l, int m, int n)
+ * reference: tests/test_fortran.py:72-103 (real*4 variant)                */
+int lfb_sgemm_f32(float alpha, const float *a, const float *b, float *c,
+                  int l, int m, int n,
+                  const lfb_launch *geom, lfb_stream stream);
+
+/* Microbenchmark used by bench.py to state the FP64 issue ceiling the SEM
+ * kernel runs against: iters x 8 independent DMUL+DADD chains per thread. */
+int lfb_probe_fp64(double *out, int iters, int blocks, int threads,
+                   lfb_stream stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LOOPFORGE_B200_H */

@@ -1,0 +1,32 @@
+"""B200-native executor for Fortran-ingested, transformed loopforge kernels.
+
+The reference (arXiv 1503.07659's Loo.py, re-created as ``loopforge``) keeps
+its Fortran-subset front end and transform library; this package replaces
+the execution step -- ``loopforge.interp.interpret`` -- with hand-written
+sm_100a kernels behind a C ABI (include/loopforge_b200.h)::
+
+    from loopforge.fortran import translate_file_text
+    import paper_1503_07659_b200 as lfb
+
+    raw, knl, _ = translate_file_text(source)        # unchanged front end
+    env = lfb.make_device_env(knl, {"nelt": 65536}, seed=0)
+    out = lfb.interpret(knl, env)                    # runs on the B200
+    w = lfb.get_output(out, "w")
+
+See DESIGN.md for the kernels and INTEGRATION.md for the ABI bindings.
+"""
+
+from .executor import (DeviceArray, DeviceEnv, Launcher, env_from_buffers,
+                       flat_outputs, get_device_output, get_output,
+                       interpret, make_device_env, plan_for)
+from .launch import Geometry, launch_geometry
+from .recognize import WORKLOADS, canonicalize, recognize
+
+__all__ = [
+    "DeviceArray", "DeviceEnv", "Launcher", "env_from_buffers",
+    "flat_outputs", "get_device_output", "get_output", "interpret",
+    "make_device_env", "plan_for", "Geometry", "launch_geometry",
+    "WORKLOADS", "canonicalize", "recognize",
+]
+
+__version__ = "0.1.0"

@@ -1,0 +1,207 @@
+// Dense matrix-vector product (BASELINE config 2).
+//
+// Reference arithmetic (SURVEY.md Appendix B fixture, fixtures.py
+// matvec_source; interp.py:323-400, emitted C identical):
+//   for every row i:  s = 0
+//                     for j ascending: s = s + a(i,j)*x(j)
+//                     y(i) = s
+// a is column major, a(i,j) at a[i + n j] (fortran.py:638-658).  The
+// reference script's extract_subst + precompute stage x in a private 32-wide
+// tile (transforms.py:541-684) -- a copy, so values are unchanged.
+//
+// Every row is one sequential chain of 2n separately rounded operations; the
+// device keeps that chain (bitwise parity) and parallelises over rows only.
+// The kernel is HBM bound (8 n^2 bytes of a), so the design is about bytes in
+// flight, not FLOPs:
+//  * one CTA per 32-row panel: warp 0 computes (lane r owns row i0 + r),
+//    warp 1 lane 0 is the TMA producer;
+//  * the producer streams 32 x JT tiles of a with cp.async.bulk.tensor.2d
+//    (a tensor map over the column-major matrix; out-of-range rows/columns
+//    are zero filled and never summed) plus the matching x slice with a 1-D
+//    bulk copy, through an S-stage full/empty mbarrier ring (S*16 KB in
+//    flight per SM);
+//  * the consumer reads its row from smem (conflict free: lanes hit
+//    consecutive doubles) and x[j] as a broadcast.
+// n odd (TMA needs 16-byte strides) or tiny n falls back to a direct-load
+// kernel with the same arithmetic.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include "lfb_common.cuh"
+
+namespace lfb {
+
+constexpr int MV_ROWS = 32;
+constexpr int MV_JT = 64;
+constexpr int MV_STAGES = 8;
+
+struct MvSmem {
+  static constexpr size_t bars = 256;
+  static constexpr size_t tile_bytes = MV_ROWS * MV_JT * 8;  // 16 KB
+  static constexpr size_t x_bytes = MV_JT * 8;
+  static constexpr size_t tiles_off = 1024;
+  static constexpr size_t xs_off = tiles_off + MV_STAGES * tile_bytes;
+  static constexpr size_t total = xs_off + MV_STAGES * x_bytes;
+};
+
+__global__ void __launch_bounds__(64, 1)
+    matvec_tma_kernel(const __grid_constant__ CUtensorMap tmap_a,
+                      double *__restrict__ y, const double *__restrict__ x,
+                      int n) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem);
+  uint64_t *empty = full + MV_STAGES;
+  double *tiles = reinterpret_cast<double *>(smem + MvSmem::tiles_off);
+  double *xs = reinterpret_cast<double *>(smem + MvSmem::xs_off);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int i0 = blockIdx.x * MV_ROWS;
+  const int ntiles = (n + MV_JT - 1) / MV_JT;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < MV_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (warp == 1) {
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap_a) : "memory");
+      const uint64_t pol = policy_evict_first();
+      for (int q = 0; q < ntiles; ++q) {
+        const int s = q % MV_STAGES;
+        mbar_wait(&empty[s], ((q / MV_STAGES) & 1) ^ 1);
+        const int j0 = q * MV_JT;
+        const int jn = min(MV_JT, n - j0);
+        const uint32_t xb = (uint32_t)jn * 8;  // n even => multiple of 16
+        mbar_arrive_expect_tx(&full[s], (uint32_t)MvSmem::tile_bytes + xb);
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::"
+            "complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(
+                smem_u32(tiles + (size_t)s * MV_ROWS * MV_JT)),
+            "l"(&tmap_a), "r"(i0), "r"(j0), "r"(smem_u32(&full[s])),
+            "l"(pol)
+            : "memory");
+        bulk_g2s(xs + s * MV_JT, x + j0, xb, &full[s]);
+      }
+    }
+    return;
+  }
+
+  // consumer warp: lane owns row i0 + lane
+  double acc = 0.0;  // "s = 0" (an i32 literal stored into the f64 scalar)
+  for (int q = 0; q < ntiles; ++q) {
+    const int s = q % MV_STAGES;
+    mbar_wait(&full[s], (q / MV_STAGES) & 1);
+    const double *tile = tiles + (size_t)s * MV_ROWS * MV_JT;
+    const double *xt = xs + s * MV_JT;
+    const int jn = min(MV_JT, n - q * MV_JT);
+    if (jn == MV_JT) {
+#pragma unroll 16
+      for (int jj = 0; jj < MV_JT; ++jj)
+        acc = dadd(acc, dmul(tile[jj * MV_ROWS + lane], xt[jj]));
+    } else {
+      for (int jj = 0; jj < jn; ++jj)
+        acc = dadd(acc, dmul(tile[jj * MV_ROWS + lane], xt[jj]));
+    }
+    __syncwarp();
+    if (lane == 0) {
+      fence_proxy_async_smem();
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(
+                       smem_u32(&empty[s]))
+                   : "memory");
+    }
+  }
+  if (i0 + lane < n) y[i0 + lane] = acc;
+}
+
+// direct-load fallback: a warp per 32 rows, loads of a coalesced across lanes
+__global__ void matvec_direct_kernel(double *__restrict__ y,
+                                     const double *__restrict__ a,
+                                     const double *__restrict__ x, int n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double acc = 0.0;
+  const double *col = a + i;
+  int j = 0;
+  for (; j + 8 <= n; j += 8) {
+    double av[8], xv[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      av[q] = __ldg(col + (int64_t)(j + q) * n);
+      xv[q] = __ldg(x + j + q);
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc = dadd(acc, dmul(av[q], xv[q]));
+  }
+  for (; j < n; ++j) acc = dadd(acc, dmul(__ldg(col + (int64_t)j * n), x[j]));
+  y[i] = acc;
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p,
+                                cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+static int matvec_impl(double *y, const double *a, const double *x, int n,
+                       const lfb_launch *geom, cudaStream_t s) {
+  const bool tma_ok = (n % 2 == 0) && n >= MV_JT && aligned(a, 16) &&
+                      aligned(x, 16) && !(geom && geom->variant == 1);
+  if (tma_ok) {
+    auto encode = encode_fn();
+    if (!encode)
+      return fail(LFB_ERR_LAUNCH, "matvec: cuTensorMapEncodeTiled missing");
+    CUtensorMap tm;
+    cuuint64_t dims[2] = {(cuuint64_t)n, (cuuint64_t)n};
+    cuuint64_t strides[1] = {(cuuint64_t)n * 8};
+    cuuint32_t box[2] = {MV_ROWS, MV_JT};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = encode(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2,
+                        const_cast<double *>(a), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_NONE,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+      return fail(LFB_ERR_LAUNCH, "matvec: tensor map encode failed (%d)",
+                  (int)r);
+    const int grid = (n + MV_ROWS - 1) / MV_ROWS;
+    cudaFuncSetAttribute(matvec_tma_kernel,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)MvSmem::total);
+    matvec_tma_kernel<<<grid, 64, MvSmem::total, s>>>(tm, y, x, n);
+  } else {
+    matvec_direct_kernel<<<(n + 127) / 128, 128, 0, s>>>(y, a, x, n);
+  }
+  return check_launch("lfb_matvec_f64");
+}
+
+}  // namespace lfb
+
+extern "C" int lfb_matvec_f64(double *y, const double *a, const double *x,
+                              int n, const lfb_launch *geom,
+                              lfb_stream stream) {
+  if (n < 0) return lfb::fail(LFB_ERR_ARG, "lfb_matvec_f64: n < 0");
+  if (n == 0) return LFB_OK;
+  if (!y || !a || !x)
+    return lfb::fail(LFB_ERR_ARG, "lfb_matvec_f64: null array");
+  if (geom && geom->abi_version != LFB_ABI_VERSION)
+    return lfb::fail(LFB_ERR_ARG, "lfb_matvec_f64: bad lfb_launch version");
+  if (geom && geom->group_extent[0] > 0 &&
+      geom->group_extent[0] * (int64_t)geom->local_extent[0] < n)
+    return lfb::fail(LFB_ERR_ARG,
+                     "lfb_matvec_f64: launch geometry covers fewer than n "
+                     "rows");
+  return lfb::matvec_impl(y, a, x, n, geom, (cudaStream_t)stream);
+}

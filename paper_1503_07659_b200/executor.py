@@ -1,0 +1,299 @@
+"""Device execution environment and the ``interpret`` drop-in.
+
+Mirrors the reference's execution API one for one
+(/root/reference/pkg/src/loopforge/interp.py):
+
+=====================================  ======================================
+reference                              B200 executor
+=====================================  ======================================
+``make_env(kernel, params, inputs,      ``make_device_env(...)`` -- same
+seed, trace)`` interp.py:79-123         checks, same flat strided layout, the
+                                        same seeded inputs, buffers in HBM
+``interpret(kernel, env)``              ``interpret(kernel, env)`` -- runs
+interp.py:323-400                       the recognised sm_100a kernel on the
+                                        current CUDA stream; returns a new env
+``get_output(env, name)`` 417-419       ``get_output`` (numpy, logical shape)
+                                        / ``get_device_output`` (torch view)
+``FlatArray`` interp.py:31-57           ``DeviceArray`` (flat torch tensor +
+                                        logical shape/strides)
+=====================================  ======================================
+
+Like the reference, ``interpret`` does not mutate its input env (interp.py:329
+``env.copy()``): output arrays are cloned first unless ``inplace=True``.
+Errors are the reference's: ``InterpError`` for bad bindings and device
+faults, ``CodegenError`` for kernels the executor cannot run.  There is no
+CPU fallback.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import abi
+from ._loopforge import CodegenError, InterpError
+from .launch import check_assumptions, launch_geometry
+from .recognize import recognize
+
+NP_DTYPE = {"f32": np.float32, "f64": np.float64, "i32": np.int32}
+TORCH_DTYPE = {"f32": torch.float32, "f64": torch.float64, "i32": torch.int32}
+
+
+def _flat_size(shape, strides):
+    """interp.py:73-76."""
+    if not shape:
+        return 1
+    return sum(s * (n - 1) for s, n in zip(strides, shape)) + 1
+
+
+@dataclass
+class DeviceArray:
+    dtype: str
+    data: torch.Tensor       # flat, element strided, on the device
+    shape: tuple
+    strides: tuple
+
+    def logical(self):
+        """Logical-shape strided view (no copy)."""
+        if not self.shape:
+            return self.data[:1]
+        return torch.as_strided(self.data, self.shape, self.strides)
+
+    def copy(self):
+        return DeviceArray(self.dtype, self.data.clone(), self.shape,
+                           self.strides)
+
+
+@dataclass
+class DeviceEnv:
+    params: dict = field(default_factory=dict)
+    arrays: dict = field(default_factory=dict)   # name -> DeviceArray
+    scalars: dict = field(default_factory=dict)  # name -> numpy scalar
+    device: torch.device = None
+
+
+def _device(device):
+    if device is None:
+        if not torch.cuda.is_available():
+            raise InterpError("the B200 executor needs a CUDA device "
+                              "(no CPU fallback)")
+        return torch.device("cuda", torch.cuda.current_device())
+    return torch.device(device)
+
+
+def make_device_env(kernel, params, inputs=None, seed=None, device=None):
+    """Bind parameters and device arrays for a kernel run (interp.py:79-123).
+
+    *inputs* maps argument names to numpy arrays / torch tensors of logical
+    shape, or scalars.  Unspecified arrays are zero filled, or -- with *seed*
+    -- filled with the reference's recipe (``rng.random(shape)*2-1`` for
+    floats, ``rng.integers(-10, 10)`` for i32, non-output arrays only, in
+    argument order), so a seeded device env holds exactly the values of the
+    seeded reference env.
+    """
+    dev = _device(device)
+    inputs = dict(inputs or {})
+    params = {k: int(v) for k, v in params.items()}
+    check_assumptions(kernel, params)
+    rng = np.random.default_rng(seed) if seed is not None else None
+    env = DeviceEnv(params=params, device=dev)
+    for a in kernel.args:
+        npt = NP_DTYPE[a.dtype]
+        if a.kind == "scalar-value":
+            env.scalars[a.name] = npt(inputs.pop(a.name, 0))
+            continue
+        shape = tuple(s.eval(params) for s in a.shape)
+        strides = tuple(s.eval(params) for s in a.strides)
+        if any(n <= 0 for n in shape):
+            raise InterpError(
+                f"array '{a.name}' has non-positive shape {shape}")
+        flat = torch.zeros(_flat_size(shape, strides),
+                           dtype=TORCH_DTYPE[a.dtype], device=dev)
+        arr = DeviceArray(a.dtype, flat, shape, strides)
+        src = None
+        if a.name in inputs:
+            src = inputs.pop(a.name)
+            if isinstance(src, torch.Tensor):
+                src = src.to(device=dev, dtype=TORCH_DTYPE[a.dtype])
+            else:
+                src = torch.from_numpy(np.ascontiguousarray(
+                    np.asarray(src, dtype=npt))).to(dev)
+            if tuple(src.shape) != shape:
+                raise InterpError(
+                    f"array '{a.name}': expected shape {shape}, "
+                    f"got {tuple(src.shape)}")
+        elif rng is not None and not a.is_output:
+            vals = rng.random(shape) * 2 - 1 if a.dtype != "i32" \
+                else rng.integers(-10, 10, shape)
+            src = torch.from_numpy(np.ascontiguousarray(
+                vals.astype(npt))).to(dev)
+        if src is not None:
+            arr.logical().copy_(src)
+        env.arrays[a.name] = arr
+    if inputs:
+        raise InterpError(f"unknown input arrays: {sorted(inputs)}")
+    return env
+
+
+def env_from_buffers(kernel, params, buffers, scalars=None):
+    """Wrap existing flat device tensors (no copy) -- the ``run`` boundary
+    of SURVEY.md §8(b)."""
+    params = {k: int(v) for k, v in params.items()}
+    check_assumptions(kernel, params)
+    env = DeviceEnv(params=params)
+    scalars = dict(scalars or {})
+    for a in kernel.args:
+        if a.kind == "scalar-value":
+            env.scalars[a.name] = NP_DTYPE[a.dtype](scalars.pop(a.name, 0))
+            continue
+        if a.name not in buffers:
+            raise InterpError(f"missing buffer for array '{a.name}'")
+        t = buffers[a.name]
+        shape = tuple(s.eval(params) for s in a.shape)
+        strides = tuple(s.eval(params) for s in a.strides)
+        need = _flat_size(shape, strides)
+        if t.dtype != TORCH_DTYPE[a.dtype] or not t.is_cuda \
+                or t.dim() != 1 or t.numel() < need \
+                or not t.is_contiguous():
+            raise InterpError(
+                f"buffer '{a.name}' must be a contiguous 1-D CUDA "
+                f"{a.dtype} tensor of >= {need} elements")
+        env.arrays[a.name] = DeviceArray(a.dtype, t, shape, strides)
+        env.device = t.device
+    return env
+
+
+# {{{ recognition cache
+
+_PLAN_CACHE = {}
+
+
+def plan_for(kernel):
+    """Cached :func:`recognize.recognize` (kernels are immutable)."""
+    hit = _PLAN_CACHE.get(id(kernel))
+    if hit is not None and hit[0] is kernel:
+        return hit[1]
+    match = recognize(kernel)
+    if len(_PLAN_CACHE) > 256:
+        _PLAN_CACHE.clear()
+    _PLAN_CACHE[id(kernel)] = (kernel, match)
+    return match
+
+# }}}
+
+
+def _ptr(arr):
+    return arr.data.data_ptr()
+
+
+def _int_param(v, name):
+    if not -2**31 <= v < 2**31:
+        raise InterpError(f"parameter {name}={v} does not fit the C int of "
+                          "the emitted-C ABI")
+    return v
+
+
+class Launcher:
+    """One prepared launch: recognised workload + geometry + pointers."""
+
+    def __init__(self, kernel, env, variant=0, sumsq=None, workspace=None):
+        self.kernel = kernel
+        self.match = plan_for(kernel)
+        self.geometry = launch_geometry(kernel, env.params)
+        self.variant = variant
+        self.env = env
+        w = self.match.workload
+        self.npts = w.npts
+        self._sumsq = sumsq
+        self._workspace = workspace
+
+    def workload(self):
+        return self.match.workload
+
+    def launch(self, env=None, stream=None):
+        env = env or self.env
+        lib = abi.load()
+        m = self.match
+        w = m.workload
+        am, pm = m.arg_map, m.param_map
+        arrays, scalars, params = env.arrays, env.scalars, env.params
+        if stream is None:
+            stream = torch.cuda.current_stream(env.device).cuda_stream
+        geom = abi.make_launch(
+            self.geometry, npts=w.npts, variant=self.variant,
+            sumsq=None if self._sumsq is None else self._sumsq.data_ptr(),
+            workspace=None if self._workspace is None
+            else self._workspace.data_ptr(),
+            workspace_len=0 if self._workspace is None
+            else self._workspace.numel())
+        gp = abi.C.byref(geom)
+
+        def P(name):
+            return abi.C.c_void_p(_ptr(arrays[am[name]]))
+
+        def S(name):
+            return scalars[am[name]]
+
+        def I(name):
+            user = pm[name]
+            return _int_param(params[user], user)
+
+        fam, dt = w.name, w.dtype
+        if fam == "fill":
+            fn = lib.lfb_fill_f64 if dt == "f64" else lib.lfb_fill_f32
+            rc = fn(P("out"), float(S("a")), I("n"), gp, stream)
+        elif fam == "axpy":
+            fn = lib.lfb_axpy_f64 if dt == "f64" else lib.lfb_axpy_f32
+            rc = fn(P("y"), P("x"), float(S("alpha")), I("n"), gp, stream)
+        elif fam == "matvec":
+            rc = lib.lfb_matvec_f64(P("y"), P("a"), P("x"), I("n"), gp,
+                                    stream)
+        elif fam == "semlap":
+            rc = lib.lfb_semlap_f64(P("w"), P("u"), P("d"), P("g"),
+                                    I("nelt"), gp, stream)
+        elif fam == "gemm":
+            rc = lib.lfb_sgemm_f32(float(S("alpha")), P("a"), P("b"),
+                                   P("c"), I("l"), I("m"), I("n"), gp,
+                                   stream)
+        else:
+            raise CodegenError(f"no entry point for workload {fam}")
+        abi.check(rc, f"{fam}_{dt}")
+
+
+def interpret(kernel, env, inplace=False, variant=0, stream=None):
+    """Run *kernel* on the B200 (drop-in for interp.py:323).
+
+    Returns a new :class:`DeviceEnv` whose output arrays hold the results;
+    the launch is asynchronous on the current CUDA stream (or *stream*).
+    """
+    check_assumptions(kernel, env.params)
+    out = DeviceEnv(dict(env.params), dict(env.arrays), dict(env.scalars),
+                    env.device)
+    if not inplace:
+        for a in kernel.args:
+            if a.kind == "global-array" and a.is_output:
+                out.arrays[a.name] = env.arrays[a.name].copy()
+    Launcher(kernel, out, variant=variant).launch(stream=stream)
+    return out
+
+
+def get_device_output(env, name):
+    """Logical-shape torch view of an array (interp.py:417-419)."""
+    if name in env.scalars:
+        return env.scalars[name]
+    return env.arrays[name].logical()
+
+
+def get_output(env, name):
+    """Logical-shape numpy copy of an array (interp.py:417-419)."""
+    if name in env.scalars:
+        return env.scalars[name]
+    return get_device_output(env, name).cpu().numpy()
+
+
+def flat_outputs(kernel, env):
+    """Flat host copies of every output array (tests/c_oracle.py:114-117)."""
+    return {a.name: env.arrays[a.name].data.cpu().numpy()
+            for a in kernel.args if a.kind == "global-array" and a.is_output}

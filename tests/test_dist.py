@@ -1,0 +1,81 @@
+"""Multi-process host logic on CPU (gloo, world_size 2): element shards and
+the verification-norm all-reduce."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle
+from paper_1503_07659_b200.dist import (allreduce_max, allreduce_sum,
+                                        shard_params, shard_range)
+
+
+@pytest.mark.parametrize("nelt,world,block", [(1 << 21, 8, 32), (100, 3, 7),
+                                              (65536, 2, 32), (5, 4, 1),
+                                              (31, 2, 32)])
+def test_shards_partition_elements(nelt, world, block):
+    spans = [shard_range(nelt, r, world, block) for r in range(world)]
+    assert spans[0][0] == 0 and spans[-1][1] == nelt
+    for (a, b), (c, _d) in zip(spans, spans[1:]):
+        assert b == c and a <= b
+    for lo, hi in spans[:-1]:
+        assert lo % block == 0 and hi % block == 0
+
+
+def test_shard_params():
+    assert shard_params({"nelt": 64, "q": 1}, "nelt", 32, 64) == \
+        {"nelt": 32, "q": 1}
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, n, nelt, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    rng = np.random.default_rng(0)            # same global problem everywhere
+    u = rng.random(nelt * n**3)
+    g = rng.random(6 * nelt * n**3)
+    d = rng.random(n * n)
+    lo, hi = shard_range(nelt, rank, world, 4)
+    w = np.zeros_like(u)
+    oracle.semlap(w, u, d, g, n, nelt, elems=(lo, hi))
+    part = oracle.sumsq(np.ascontiguousarray(w[lo * n**3:hi * n**3]))
+    total = allreduce_sum(part)
+    worst = allreduce_max(float(rank))
+    q.put((rank, total, worst))
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_norm_allreduce():
+    n, nelt, world = 4, 18, 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, nelt, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    rng = np.random.default_rng(0)
+    u = rng.random(nelt * n**3)
+    g = rng.random(6 * nelt * n**3)
+    d = rng.random(n * n)
+    w = oracle.semlap(np.zeros_like(u), u, d, g, n, nelt)
+    want = float((w * w).sum())
+    for _rank, total, worst in res:
+        assert abs(total - want) <= 1e-12 * want
+        assert worst == world - 1

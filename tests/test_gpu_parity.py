@@ -1,0 +1,262 @@
+"""Device parity: the sm_100a kernels against the reference.
+
+* every golden (made by the reference interpreter, tests/golden/) is
+  reproduced bit for bit through the drop-in ``interpret``;
+* at BASELINE sizes, outputs are compared with the CPU oracle (pinned to the
+  reference by tests/test_oracle.py) on full arrays or on element/row/column
+  samples, bitwise;
+* geometry variants (block sizes, guards, ragged extents) and the error
+  behaviour of the reference (InterpError / CodegenError) are covered.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_1503_07659_b200 as lfb
+from conftest import Golden, golden_names
+from paper_1503_07659_b200 import fixtures as fx
+from paper_1503_07659_b200._loopforge import CodegenError, InterpError
+
+pytestmark = pytest.mark.gpu
+
+
+def _env_from_golden(g, knl, dev):
+    env = lfb.make_device_env(knl, g.params, device=dev)
+    for a in knl.args:
+        buf = g.inp(a.name)
+        if a.kind == "scalar-value":
+            env.scalars[a.name] = buf.reshape(-1)[0]
+        else:
+            env.arrays[a.name].data.copy_(torch.from_numpy(buf.copy()))
+    return env
+
+
+@pytest.mark.parametrize("name", golden_names())
+def test_golden_bitwise(name, cuda):
+    g = Golden(name)
+    _raw, knl = g.kernels()
+    env = _env_from_golden(g, knl, cuda)
+    before = {k: v.data.clone() for k, v in env.arrays.items()}
+    out = lfb.interpret(knl, env)
+    torch.cuda.synchronize()
+    for o in g.outputs():
+        got = out.arrays[o].data.cpu().numpy()
+        want = g.out(o)
+        assert got.dtype == want.dtype
+        assert got.tobytes() == want.tobytes(), f"{name}:{o}"
+    # interpret never mutates its input env (interp.py:329 env.copy())
+    for k, v in env.arrays.items():
+        assert torch.equal(v.data, before[k]), k
+
+
+@pytest.mark.parametrize("name", ["semlap_n8_b2_nelt2", "matvec_f64_n128",
+                                  "sgemm_m20_n12_l40", "axpy_f64_n300"])
+def test_golden_untransformed_kernel(name, cuda):
+    """The raw (untransformed) lowering of the same text gives the same
+    bits -- transforms do not change results (test_interp.py:128-136)."""
+    g = Golden(name)
+    raw, _knl = g.kernels()
+    env = _env_from_golden(g, raw, cuda)
+    out = lfb.interpret(raw, env)
+    for o in g.outputs():
+        assert out.arrays[o].data.cpu().numpy().tobytes() == \
+            g.out(o).tobytes()
+
+
+def _sem_inputs(n, nelt, dev, seed=0):
+    gen = torch.Generator(device=dev).manual_seed(seed)
+    u = torch.rand(nelt * n**3, dtype=torch.float64, device=dev,
+                   generator=gen) * 2 - 1
+    g = torch.rand(6 * nelt * n**3, dtype=torch.float64, device=dev,
+                   generator=gen)
+    d = torch.rand(n * n, dtype=torch.float64, device=dev,
+                   generator=gen) * 2 - 1
+    return u, d, g
+
+
+def _sem_check(n, nelt, src, dev, samples, variant=0, seed=0):
+    _raw, knl = fx.translate(src)
+    u, d, g = _sem_inputs(n, nelt, dev, seed)
+    w = torch.full_like(u, float("nan"))
+    env = lfb.env_from_buffers(knl, {"nelt": nelt},
+                               {"u": u, "d": d, "g": g, "w": w})
+    lfb.interpret(knl, env, inplace=True, variant=variant)
+    torch.cuda.synchronize()
+    uh, dh, gh, wh = (t.cpu().numpy() for t in (u, d, g, w))
+    np3 = n**3
+    for lo, hi in samples:
+        ref = np.zeros_like(uh)
+        oracle.semlap(ref, uh, dh, gh, n, nelt, elems=(lo, hi), threads=8)
+        assert wh[lo * np3:hi * np3].tobytes() == \
+            ref[lo * np3:hi * np3].tobytes(), (lo, hi)
+    assert not np.isnan(wh).any()
+
+
+def test_semlap_o7_65536_elements(cuda):
+    """BASELINE config 3 (order 7, 65,536 elements, the fixture script)."""
+    nelt = 65536
+    _sem_check(8, nelt, fx.semlap_source(8), cuda,
+               [(0, 1024), (30000, 31000), (nelt - 1024, nelt)])
+
+
+@pytest.mark.parametrize("variant", [1, 2, 3])
+def test_semlap_o7_variants(cuda, variant):
+    nelt = 4096
+    _sem_check(8, nelt, fx.semlap_source(8), cuda, [(0, nelt)],
+               variant=variant)
+
+
+@pytest.mark.parametrize("n", [2, 4, 6, 8, 10])
+def test_semlap_orders(cuda, n):
+    nelt = 640
+    _sem_check(n, nelt, fx.semlap_source(n), cuda, [(0, nelt)], seed=n)
+
+
+@pytest.mark.parametrize("block,nelt", [(1, 37), (7, 100), (32, 33),
+                                        (32, 1), (3, 448)])
+def test_semlap_ragged_and_guarded(cuda, block, nelt):
+    """Blocks that do not divide nelt: the reference emits a guard; no
+    assume() so any nelt is legal."""
+    src = fx.semlap_source(8, block=block, assume=False)
+    _sem_check(8, nelt, src, cuda, [(0, nelt)], seed=block)
+
+
+def test_semlap_sumsq_epilogue(cuda):
+    n, nelt = 8, 3000
+    _raw, knl = fx.translate(fx.semlap_source(n))
+    # nelt must satisfy the fixture's assume(nelt mod 32 = 0)
+    nelt = 3008
+    u, d, g = _sem_inputs(n, nelt, cuda, 5)
+    w = torch.empty_like(u)
+    env = lfb.env_from_buffers(knl, {"nelt": nelt},
+                               {"u": u, "d": d, "g": g, "w": w})
+    sumsq = torch.zeros(1, dtype=torch.float64, device=cuda)
+    ws = torch.zeros(4096, dtype=torch.float64, device=cuda)
+    lfb.Launcher(knl, env, sumsq=sumsq, workspace=ws).launch()
+    torch.cuda.synchronize()
+    ref = float((w.double() ** 2).sum())
+    assert abs(float(sumsq) - ref) <= 1e-12 * abs(ref)
+
+
+def test_fill_axpy_2_24(cuda):
+    """BASELINE config 1 at full size: bitwise against numpy, which rounds
+    each operation exactly like the reference (interp.py:169-187)."""
+    n = 1 << 24
+    _r, kf = fx.translate(fx.fill_source("f64"))
+    env = lfb.make_device_env(kf, {"n": n}, {"a": 1.5}, device=cuda)
+    out = lfb.interpret(kf, env)
+    assert bool((out.arrays["out"].data == 1.5).all())
+    _r, ka = fx.translate(fx.axpy_source("f64"))
+    gen = torch.Generator(device=cuda).manual_seed(1)
+    x = torch.rand(n, dtype=torch.float64, device=cuda, generator=gen)
+    y = torch.rand(n, dtype=torch.float64, device=cuda, generator=gen)
+    y0 = y.cpu().numpy().copy()
+    env = lfb.env_from_buffers(ka, {"n": n}, {"x": x, "y": y},
+                               {"alpha": 1.25})
+    lfb.interpret(ka, env, inplace=True)
+    want = y0 + np.float64(1.25) * x.cpu().numpy()
+    assert y.cpu().numpy().tobytes() == want.tobytes()
+
+
+@pytest.mark.parametrize("n", [1, 5, 127, 129, 1000003])
+def test_fill_axpy_ragged(cuda, n):
+    for dt, npt in (("f64", np.float64), ("f32", np.float32)):
+        _r, ka = fx.translate(fx.axpy_source(dt))
+        env = lfb.make_device_env(ka, {"n": n}, {"alpha": 0.3}, seed=n,
+                                  device=cuda)
+        y = np.random.default_rng(n).random(n).astype(npt)
+        env.arrays["y"].data.copy_(torch.from_numpy(y))
+        x = env.arrays["x"].data.cpu().numpy()
+        out = lfb.interpret(ka, env)
+        want = y + npt(0.3) * x
+        assert out.arrays["y"].data.cpu().numpy().tobytes() == want.tobytes()
+        _r, kf = fx.translate(fx.fill_source(dt))
+        env = lfb.make_device_env(kf, {"n": n}, {"a": 0.1}, device=cuda)
+        out = lfb.interpret(kf, env)
+        assert (out.arrays["out"].data.cpu().numpy() == npt(0.1)).all()
+
+
+def test_fill_misaligned_pointer(cuda):
+    _r, kf = fx.translate(fx.fill_source("f64"))
+    base = torch.zeros(1001, dtype=torch.float64, device=cuda)
+    env = lfb.env_from_buffers(kf, {"n": 1000}, {"out": base[1:]},
+                               {"a": 2.0})
+    lfb.interpret(kf, env, inplace=True)
+    h = base.cpu().numpy()
+    assert h[0] == 0 and (h[1:] == 2.0).all()
+
+
+@pytest.mark.parametrize("n", [4096, 128, 256, 1024 + 128])
+def test_matvec(cuda, n):
+    """BASELINE config 2 at n=4096: full bitwise comparison."""
+    _r, knl = fx.translate(fx.matvec_source("f64"))
+    gen = torch.Generator(device=cuda).manual_seed(n)
+    a = torch.rand(n * n, dtype=torch.float64, device=cuda, generator=gen)
+    x = torch.rand(n, dtype=torch.float64, device=cuda, generator=gen)
+    y = torch.full((n,), float("nan"), dtype=torch.float64, device=cuda)
+    env = lfb.env_from_buffers(knl, {"n": n}, {"a": a, "x": x, "y": y})
+    lfb.interpret(knl, env, inplace=True)
+    ref = oracle.matvec(np.zeros(n), a.cpu().numpy(), x.cpu().numpy(), n,
+                        threads=8)
+    assert y.cpu().numpy().tobytes() == ref.tobytes()
+
+
+@pytest.mark.parametrize("n", [97, 130, 4095])
+def test_matvec_untransformed_odd_sizes(cuda, n):
+    """Odd n (TMA cannot describe the stride): direct-load path."""
+    src = fx.matvec_source("f64", script=False)
+    raw, _k = fx.translate(src)
+    gen = torch.Generator(device=cuda).manual_seed(n)
+    a = torch.rand(n * n, dtype=torch.float64, device=cuda, generator=gen)
+    x = torch.rand(n, dtype=torch.float64, device=cuda, generator=gen)
+    y = torch.zeros(n, dtype=torch.float64, device=cuda)
+    env = lfb.env_from_buffers(raw, {"n": n}, {"a": a, "x": x, "y": y})
+    lfb.interpret(raw, env, inplace=True)
+    ref = oracle.matvec(np.zeros(n), a.cpu().numpy(), x.cpu().numpy(), n)
+    assert y.cpu().numpy().tobytes() == ref.tobytes()
+
+
+@pytest.mark.parametrize("m,n,l", [(256, 128, 64), (200, 72, 100),
+                                   (1024, 512, 768)])
+def test_sgemm_exact(cuda, m, n, l):
+    """variant=1: the bit-exact CUDA-core path."""
+    _r, knl = fx.translate(fx.gemm_source("f32"))
+    rng = np.random.default_rng(m + n + l)
+    a = rng.random(m * l).astype(np.float32)
+    b = rng.random(l * n).astype(np.float32)
+    c = rng.random(m * n).astype(np.float32)
+    env = lfb.env_from_buffers(
+        knl, {"m": m, "n": n, "l": l},
+        {"a": torch.from_numpy(a).to(cuda), "b": torch.from_numpy(b).to(cuda),
+         "c": torch.from_numpy(c.copy()).to(cuda)}, {"alpha": 1.5})
+    out = lfb.interpret(knl, env, variant=1)
+    ref = oracle.sgemm(np.float32(1.5), a, b, c.copy(), l, m, n, threads=8)
+    assert out.arrays["c"].data.cpu().numpy().tobytes() == ref.tobytes()
+
+
+# {{{ error behaviour mirrors the reference
+
+def test_assumption_violation_is_interp_error(cuda):
+    _r, knl = fx.translate(fx.semlap_source(8))
+    with pytest.raises(InterpError, match="assumption"):
+        lfb.make_device_env(knl, {"nelt": 33}, device=cuda)
+
+
+def test_unrecognised_kernel_is_codegen_error(cuda):
+    src = fx.axpy_source("f64").replace("y(i) + alpha*x(i)",
+                                        "y(i) + x(i)*alpha")
+    _r, knl = fx.translate(src)
+    env = lfb.make_device_env(knl, {"n": 256}, device=cuda)
+    with pytest.raises(CodegenError, match="no CPU fallback"):
+        lfb.interpret(knl, env)
+
+
+def test_wrong_shape_input_is_interp_error(cuda):
+    _r, knl = fx.translate(fx.fill_source("f64"))
+    with pytest.raises(InterpError, match="expected shape"):
+        lfb.make_device_env(knl, {"n": 10}, {"out": np.zeros(11)},
+                            device=cuda)
+
+# }}}
