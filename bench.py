@@ -3,20 +3,21 @@
 Default workload = BASELINE config 4: SEM Laplacian, order 7 (n = 8 points
 per direction), fp64, 2^21 = 2,097,152 elements, the Appendix-A fixture with
 its transform script (split_iname e by 32 -> g.0/l.0, assume, extract_subst),
-element-sharded over the ranks (strong scaling: the 2M elements are split).
+element-sharded over the ranks (the 2M elements are split: strong scaling).
 One step = one execution of the transformed kernel over every element of the
 rank's shard, inputs resident in HBM (64 GiB at N=1 -- far above the 126 MB
 L2, so no flush is needed between steps).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
-                    [--workload sem2m|sem65k|fill|axpy|matvec|sgemm|sweep]
+    python bench.py --workload sem65k|fill|axpy|matvec|sgemm|sweep   (others)
 
 Prints ONE JSON line on rank 0 (the driver contract): value = whole-job
-GDOF/s (nelt * n^3 / max-over-ranks step time), the roofline of the SEM
-kernel against the measured HBM copy bandwidth, the CPU baseline (the
-reference's own emitted C, oracle/_ref, on the host cores), the end-to-end
-number through the public API with host buffers, SM clocks sampled during
-the timed region, and the number of our kernel launches.
+GDOF/s (nelt * n^3 / max-over-ranks step time); the roofline of the SEM
+kernel (algorithmic 64 n^3 bytes/element, over the CUDA-event
+launch time) against the measured HBM copy bandwidth; the CPU baseline (the
+reference's own emitted C, oracle/_ref, on the host cores); the end-to-end
+number through the public API with host buffers; SM clocks sampled during the
+timed region; the number of our kernel launches.
 """
 
 from __future__ import annotations
@@ -41,24 +42,23 @@ def _peaks():
     try:
         with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
             p = json.load(f)
-        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def _traffic(workload):
-    """Per-launch DRAM bytes of the dominant kernel from the committed ncu
-    capture (profiles/ncu_summary.json), or None."""
+def _traffic(key):
+    """Per-launch DRAM bytes (dram__bytes_read.sum + write) of the dominant
+    kernel from the committed ncu --set full capture, or None."""
     try:
         with open(os.path.join(REPO, "profiles", "ncu_summary.json")) as f:
-            s = json.load(f)
-        return s.get(workload, {}).get("dram_bytes_per_launch")
+            return json.load(f).get(key, {}).get("dram_bytes_per_launch")
     except Exception:
         return None
 
 
 class Clocks:
-    """Sample nvidia-smi during the timed region (B200_PROFILING.md)."""
+    """nvidia-smi samples during the timed region (B200_PROFILING.md)."""
 
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,"
          "clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
@@ -76,10 +76,10 @@ class Clocks:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}",
                  f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                 "-lms", "100"],
+                 "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
+            threading.Thread(target=self._read, daemon=True).start()
+            time.sleep(0.3)  # let the sampler start before the timed region
         except Exception:
             self.proc = None
         return self
@@ -90,6 +90,7 @@ class Clocks:
 
     def __exit__(self, *exc):
         if self.proc:
+            time.sleep(0.1)
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
@@ -97,7 +98,7 @@ class Clocks:
                 self.proc.kill()
 
     def summary(self):
-        sm, mx, reasons = [], 0, set()
+        sm, mx, reasons, power = [], 0.0, set(), []
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown",
                  "sw_power_cap"]
         for ln in self.lines:
@@ -107,6 +108,7 @@ class Clocks:
             try:
                 sm.append(float(parts[1]))
                 mx = max(mx, float(parts[2]))
+                power.append(float(parts[3]))
             except ValueError:
                 continue
             for nm, v in zip(names, parts[5:9]):
@@ -116,7 +118,8 @@ class Clocks:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [],
                     "samples": 0}
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm),
+                "power_w_max": max(power) if power else None}
 
 
 # {{{ distributed plumbing
@@ -127,13 +130,13 @@ def dist_init(n_gpus):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world != n_gpus and world > 1:
+    if world > 1 and world != n_gpus:
         raise SystemExit(f"--gpus {n_gpus} but WORLD_SIZE={world}")
-    if torch.cuda.is_available():
-        torch.cuda.set_device(local)
+    torch.cuda.set_device(local)
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist.init_process_group("nccl",
+                                device_id=torch.device("cuda", local))
     return rank, world, local
 
 
@@ -149,90 +152,116 @@ def max_over_ranks(x, world):
     from paper_1503_07659_b200.dist import allreduce_max
     return allreduce_max(x)
 
+
+def timed(fn, steps, warmup, world, local):
+    """W untimed steps, then K steps between barrier+synchronize pairs,
+    CUDA events on the launching stream, clocks sampled throughout.
+    Returns (max-over-ranks ms/step, this rank's ms/step, clocks)."""
+    import torch
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        barrier(world)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(steps):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier(world)
+    ms_local = e0.elapsed_time(e1) / steps
+    return max_over_ranks(ms_local, world), ms_local, clk.summary()
+
 # }}}
 
 
-def sem_workload(args, rank, world, local):
+# {{{ SEM (default)
+
+def sem_buffers(n, nelt, dev, seed):
+    import torch
+    np3 = n ** 3
+    gen = torch.Generator(device=dev).manual_seed(seed)
+    u = torch.empty(nelt * np3, dtype=torch.float64, device=dev)
+    g = torch.empty(6 * nelt * np3, dtype=torch.float64, device=dev)
+    CH = 1 << 26
+    for t, lo, hi in ((u, -1.0, 1.0), (g, 0.0, 1.0)):
+        for s in range(0, t.numel(), CH):
+            t[s:s + CH].uniform_(lo, hi, generator=gen)
+    d = torch.rand(n * n, dtype=torch.float64, device=dev,
+                   generator=gen) * 2 - 1
+    w = torch.empty_like(u)
+    return u, d, g, w
+
+
+def sem_bench(args, rank, world, local):
     import numpy as np
     import torch
 
     import paper_1503_07659_b200 as lfb
+    from paper_1503_07659_b200 import abi
     from paper_1503_07659_b200 import fixtures as fx
     from paper_1503_07659_b200.dist import allreduce_sum, shard_range
 
-    n = args.npts
-    nelt_total = args.nelt
-    block = 32
-    src = fx.semlap_source(n, block=block)
-    _raw, knl = fx.translate(src, "semlap.f")
+    n, nelt_total, block = args.npts, args.nelt, 32
+    _raw, knl = fx.translate(fx.semlap_source(n, block=block), "semlap.f")
     lo, hi = shard_range(nelt_total, rank, world, block)
     nelt = hi - lo
     dev = torch.device("cuda", local)
     np3 = n ** 3
-
-    # synthetic inputs, generated per shard on the device (per-shard seeds)
-    gen = torch.Generator(device=dev).manual_seed(1000 + rank)
-    u = torch.empty(nelt * np3, dtype=torch.float64, device=dev)
-    g = torch.empty(6 * nelt * np3, dtype=torch.float64, device=dev)
-    CH = 1 << 26
-    for t in (u, g):
-        for s in range(0, t.numel(), CH):
-            v = t[s:s + CH]
-            v.uniform_(0.0, 1.0, generator=gen)
-    u.mul_(2).sub_(1)
-    d = torch.rand(n * n, dtype=torch.float64, device=dev,
-                   generator=gen) * 2 - 1
-    w = torch.empty_like(u)
+    u, d, g, w = sem_buffers(n, nelt, dev, 1000 + rank)
     env = lfb.env_from_buffers(knl, {"nelt": nelt},
                                {"u": u, "d": d, "g": g, "w": w})
     launcher = lfb.Launcher(knl, env, variant=args.variant)
-    stream = torch.cuda.current_stream(dev)
 
-    for _ in range(args.warmup):
-        launcher.launch()
-    torch.cuda.synchronize()
-    barrier(world)
-    torch.cuda.synchronize()
-    ev0 = torch.cuda.Event(enable_timing=True)
-    ev1 = torch.cuda.Event(enable_timing=True)
-    with Clocks(local) as clk:
-        ev0.record(stream)
-        for _ in range(args.steps):
-            launcher.launch()
-        ev1.record(stream)
-        torch.cuda.synchronize()
-    barrier(world)
-    ms_local = ev0.elapsed_time(ev1) / args.steps
-    ms = max_over_ranks(ms_local, world)
-    dofs = nelt_total * np3
-    value = dofs / (ms * 1e-3) / 1e9
-
-    # roofline of the SEM kernel: algorithmic 64 n^3 bytes per element
-    # (u + 6 g read, w written) / launch duration
+    ms, ms_local, clocks = timed(launcher.launch, args.steps, args.warmup,
+                                 world, local)
+    value = nelt_total * np3 / (ms * 1e-3) / 1e9
     bytes_per_launch = 64 * np3 * nelt
     achieved = bytes_per_launch / (ms_local * 1e-3) / 1e9
     peak, peak_src = _peaks()
 
-    # verification (outside the timed region): fused sum(w^2) epilogue +
-    # NCCL all-reduce, and a bitwise sample against the CPU oracle
-    ws = torch.zeros(max(1, int(lfb_ws(n, nelt))), dtype=torch.float64,
-                     device=dev)
+    # the same HBM access mix without the arithmetic, same buffers: the
+    # streaming ceiling at this footprint (context for roofline.frac)
+    lib = abi.load()
+    st = torch.cuda.current_stream(dev).cuda_stream
+    for _ in range(2):
+        lib.lfb_probe_stream(w.data_ptr(), u.data_ptr(), g.data_ptr(),
+                             nelt * np3, st)
+    p0 = torch.cuda.Event(enable_timing=True)
+    p1 = torch.cuda.Event(enable_timing=True)
+    p0.record()
+    for _ in range(5):
+        lib.lfb_probe_stream(w.data_ptr(), u.data_ptr(), g.data_ptr(),
+                             nelt * np3, st)
+    p1.record()
+    torch.cuda.synchronize()
+    probe_gbs = bytes_per_launch / (p0.elapsed_time(p1) / 5 * 1e-3) / 1e9
+
+    # verification, outside the timed region: fused sum(w^2) epilogue + one
+    # NCCL all-reduce (SURVEY.md §8(e)), and a bitwise sample vs the oracle
+    ws = torch.zeros(max(1, int(abi.load().lfb_semlap_workspace(n, nelt,
+                                                                None))),
+                     dtype=torch.float64, device=dev)
     ss = torch.zeros(1, dtype=torch.float64, device=dev)
     lfb.Launcher(knl, env, sumsq=ss, workspace=ws).launch()
     torch.cuda.synchronize()
-    norm2 = allreduce_sum(float(ss.item()))
-    verify = {"sumsq_allreduced": norm2}
+    verify = {"sumsq_allreduced": allreduce_sum(float(ss.item()))}
     if not args.no_verify:
         sys.path.insert(0, os.path.join(REPO, "oracle"))
         import oracle
         ns = min(nelt, 512)
-        uh = u[:ns * np3].cpu().numpy()
-        gh = g[:6 * ns * np3].cpu().numpy()
-        dh = d.cpu().numpy()
-        ref = oracle.semlap(np.zeros_like(uh), uh, dh, gh, n, ns, threads=8)
-        verify["sample_bitwise"] = bool(
-            w[:ns * np3].cpu().numpy().tobytes() == ref.tobytes())
-        verify["sample_elements"] = ns
+        for tag, e0 in (("head", 0), ("tail", nelt - ns)):
+            uh = u[e0 * np3:(e0 + ns) * np3].cpu().numpy()
+            gh = g[6 * e0 * np3:6 * (e0 + ns) * np3].cpu().numpy()
+            ref = oracle.semlap(np.zeros_like(uh), uh, d.cpu().numpy(), gh,
+                                n, ns, threads=8)
+            verify[f"bitwise_{tag}_{ns}_elements"] = bool(
+                w[e0 * np3:(e0 + ns) * np3].cpu().numpy().tobytes()
+                == ref.tobytes())
 
     res = {
         "metric": METRIC, "value": value, "unit": "GDOF/s",
@@ -240,89 +269,123 @@ def sem_workload(args, rank, world, local):
         "config": {"workload": f"semlap order {n - 1} (n={n}) fp64, "
                                f"{nelt_total} elements, element-sharded "
                                f"over {world} GPU(s); fixture script "
-                               "split_iname(e,32,g.0,l.0)+assume+"
+                               "split_iname(e,32,g.0,l.0) + assume + "
                                "extract_subst(gf)",
                    "nelt": nelt_total, "npts": n, "block": block,
                    "parallelism": f"element shards x{world}",
-                   "l2": "inputs 64 B/dof >> 126 MB L2; no flush needed",
+                   "l2": "no flush: inputs 56 B/dof >> 126 MB L2",
                    "variant": args.variant},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": _traffic("semlap_n8"),
+                     "traffic": _traffic(f"semlap_n{n}"),
                      "peak_source": peak_src,
-                     "algorithmic_bytes_per_launch": bytes_per_launch},
-        "gpu_launches": args.steps,
-        "verify": verify,
+                     "algorithmic_bytes_per_launch": bytes_per_launch,
+                     "kernel": "semlap_kernel (1 launch per step)",
+                     "stream_probe_gbs": probe_gbs,
+                     "stream_probe_note": "same buffers, same bytes, no "
+                                          "arithmetic (lfb_probe_stream)"},
+        "clocks": clocks, "gpu_launches": args.steps, "verify": verify,
     }
-    return res, launcher, env, (u, d, g, w), knl
+    del env, launcher, u, d, g, w, ws
+    torch.cuda.empty_cache()
+    return res, knl
 
 
-def lfb_ws(n, nelt):
-    from paper_1503_07659_b200 import abi
-    return abi.load().lfb_semlap_workspace(n, nelt, None)
-
-
-def sem_e2e(args, knl, n, nelt_e2e, dev):
-    """Same metric through the public API with HOST buffers: every step
-    copies u, g, d from pinned host memory, runs interpret(), and copies w
-    back."""
+def sem_e2e(knl, n, nelt, dev, steps, chunk=1 << 17):
+    """Same metric through the public API with HOST buffers.  Every step:
+    H2D of all kernel inputs (u, g, d) from pinned host memory, interpret(),
+    D2H of the output w.  The elements are processed in chunks (each chunk
+    is an SEM problem on a slice; elements are independent) on two streams
+    so PCIe copies overlap the kernel."""
     import torch
 
     import paper_1503_07659_b200 as lfb
     np3 = n ** 3
-    hu = torch.empty(nelt_e2e * np3, dtype=torch.float64, pin_memory=True)
-    hg = torch.empty(6 * nelt_e2e * np3, dtype=torch.float64,
-                     pin_memory=True)
-    hd = torch.rand(n * n, dtype=torch.float64).pin_memory()
-    hw = torch.empty_like(hu).pin_memory()
-    hu.uniform_(-1, 1)
-    hg.uniform_(0, 1)
-    du = torch.empty_like(hu, device=dev)
-    dg = torch.empty_like(hg, device=dev)
-    dd = torch.empty_like(hd, device=dev)
-    dw = torch.empty_like(hu, device=dev)
-    env = lfb.env_from_buffers(knl, {"nelt": nelt_e2e},
-                               {"u": du, "d": dd, "g": dg, "w": dw})
-    stream = torch.cuda.current_stream(dev)
+    hu = torch.empty(nelt * np3, dtype=torch.float64, pin_memory=True)
+    hg = torch.empty(6 * nelt * np3, dtype=torch.float64, pin_memory=True)
+    hw = torch.empty(nelt * np3, dtype=torch.float64, pin_memory=True)
+    # synthetic host data: generate on the device chunk-wise, copy down
+    gen = torch.Generator(device=dev).manual_seed(7)
+    for h, sz, lo in ((hu, chunk * np3, -1.0), (hg, 6 * chunk * np3, 0.0)):
+        for s in range(0, h.numel(), sz):
+            v = h[s:s + sz]
+            v.copy_(torch.empty(v.numel(), dtype=torch.float64, device=dev)
+                    .uniform_(lo, 1.0, generator=gen))
+    hd = (torch.rand(n * n, dtype=torch.float64) * 2 - 1).pin_memory()
+    streams = [torch.cuda.Stream(dev) for _ in range(2)]
+    bufs = []
+    for _ in streams:
+        bufs.append({"u": torch.empty(chunk * np3, dtype=torch.float64,
+                                      device=dev),
+                     "g": torch.empty(6 * chunk * np3, dtype=torch.float64,
+                                      device=dev),
+                     "w": torch.empty(chunk * np3, dtype=torch.float64,
+                                      device=dev),
+                     "d": torch.empty(n * n, dtype=torch.float64,
+                                      device=dev)})
+    chunks = [(s, min(nelt, s + chunk)) for s in range(0, nelt, chunk)]
+    launches = [0]
 
     def step():
-        du.copy_(hu, non_blocking=True)
-        dg.copy_(hg, non_blocking=True)
-        dd.copy_(hd, non_blocking=True)
-        lfb.interpret(knl, env, inplace=True)
-        hw.copy_(dw, non_blocking=True)
+        for c, (e0, e1) in enumerate(chunks):
+            st, b = streams[c % 2], bufs[c % 2]
+            m = e1 - e0
+            with torch.cuda.stream(st):
+                b["u"][:m * np3].copy_(hu[e0 * np3:e1 * np3],
+                                       non_blocking=True)
+                b["g"][:6 * m * np3].copy_(hg[6 * e0 * np3:6 * e1 * np3],
+                                           non_blocking=True)
+                b["d"].copy_(hd, non_blocking=True)
+                env = lfb.env_from_buffers(
+                    knl, {"nelt": m}, {"u": b["u"], "g": b["g"],
+                                       "w": b["w"], "d": b["d"]})
+                lfb.interpret(knl, env, inplace=True)
+                launches[0] += 1
+                hw[e0 * np3:e1 * np3].copy_(b["w"][:m * np3],
+                                            non_blocking=True)
 
-    for _ in range(2):
-        step()
+    cur = torch.cuda.current_stream(dev)
+
+    def run(k):
+        for s in streams:
+            s.wait_stream(cur)
+        for _ in range(k):
+            step()
+        for s in streams:
+            cur.wait_stream(s)
+
+    run(1)
     torch.cuda.synchronize()
+    launches[0] = 0
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
-    steps = max(2, min(args.steps, 5))
-    e0.record(stream)
-    for _ in range(steps):
-        step()
-    e1.record(stream)
+    e0.record(cur)
+    run(steps)
+    e1.record(cur)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / steps
-    return {"value": nelt_e2e * np3 / (ms * 1e-3) / 1e9, "unit": "GDOF/s",
-            "h2d_bytes_per_step": (hu.numel() + hg.numel() + hd.numel()) * 8,
+    return {"value": nelt * np3 / (ms * 1e-3) / 1e9, "unit": "GDOF/s",
+            "h2d_bytes_per_step": (hu.numel() + hg.numel()) * 8
+            + len(chunks) * hd.numel() * 8,
             "d2h_bytes_per_step": hw.numel() * 8,
-            "nelt": nelt_e2e, "ms_per_step": ms,
-            "api": "paper_1503_07659_b200.interpret (ctypes C-ABI "
-                   "lfb_semlap_f64)"}
+            "ms_per_step": ms, "steps": steps,
+            "gpu_launches": launches[0],
+            "api": "paper_1503_07659_b200.interpret -> lfb_semlap_f64 "
+                   f"(ctypes C-ABI), {len(chunks)} chunks of {chunk} "
+                   "elements on 2 streams"}
 
 
-def cpu_reference_rate(n, sample_elems, threads, min_seconds=10.0):
-    """The reference's own emitted C (oracle/_ref; compiled cc -std=c99 -O1
-    as tests/c_oracle.py:96) on host cores, element chunks <= 699,050 (its
-    int indexing) and multiples of 32 (its assume(nelt mod 32 = 0))."""
-    import ctypes as C
+def cpu_reference(n, sample_elems, threads, min_seconds):
+    """The reference's own emitted C for the same transformed kernel
+    (oracle/_ref, compiled cc -std=c99 -O1 like tests/c_oracle.py:96) on the
+    host cores: element chunks (<= 699,050, multiples of 32 -- its int
+    indexing and its assume(nelt mod 32 = 0)) on `threads` threads."""
     import concurrent.futures as cf
+    import ctypes as C
 
     import numpy as np
     sys.path.insert(0, os.path.join(REPO, "oracle"))
     import oracle
-    kind = "reference"
     np3 = n ** 3
     rng = np.random.default_rng(0)
     u = rng.random(sample_elems * np3) * 2 - 1
@@ -330,59 +393,155 @@ def cpu_reference_rate(n, sample_elems, threads, min_seconds=10.0):
     d = rng.random(n * n) * 2 - 1
     w = np.zeros_like(u)
     if oracle.have_ref():
+        kind = "reference"
         P, I = C.c_void_p, C.c_int
         fn = oracle.ref_fn(f"ref_semlap_n{n}", [P, P, P, P, I])
 
         def run(e0, e1):
-            off = e0 * np3
-            fn(C.c_void_p(w.ctypes.data + off * 8),
-               C.c_void_p(u.ctypes.data + off * 8),
+            fn(C.c_void_p(w.ctypes.data + e0 * np3 * 8),
+               C.c_void_p(u.ctypes.data + e0 * np3 * 8),
                d.ctypes.data_as(P),
-               C.c_void_p(g.ctypes.data + 6 * off * 8), e1 - e0)
+               C.c_void_p(g.ctypes.data + 6 * e0 * np3 * 8), e1 - e0)
     else:
         kind = "port"
 
         def run(e0, e1):
             oracle.semlap(w, u, d, g, n, sample_elems, elems=(e0, e1))
-    per = sample_elems // threads // 32 * 32
-    cuts = [t * per for t in range(threads)] + [sample_elems]
+    per = max(32, sample_elems // threads // 32 * 32)
+    cuts = list(range(0, sample_elems, per)) + [sample_elems]
     t0 = time.perf_counter()
     reps = 0
-    while True:
-        with cf.ThreadPoolExecutor(threads) as pool:
-            list(pool.map(lambda t: run(cuts[t], cuts[t + 1]),
-                          range(threads)))
-        reps += 1
-        if time.perf_counter() - t0 >= min_seconds:
-            break
+    with cf.ThreadPoolExecutor(threads) as pool:
+        while True:
+            list(pool.map(lambda c: run(cuts[c], cuts[c + 1]),
+                          range(len(cuts) - 1)))
+            reps += 1
+            if time.perf_counter() - t0 >= min_seconds:
+                break
     dt = (time.perf_counter() - t0) / reps
     return {"value": sample_elems * np3 / dt / 1e9, "unit": "GDOF/s",
             "cores": threads, "kind": kind,
-            "sample": f"{sample_elems} elements of the same workload "
-                      f"(n={n}), {reps} rep(s), "
-                      f"{'reference emitted C -std=c99 -O1' if kind == 'reference' else 'oracle port'}, "
-                      f"{threads} thread(s)"}
+            "sample": f"{sample_elems} elements (n={n}) of the same "
+                      f"workload x {reps} rep(s); "
+                      + ("the reference's emitted C (codegen.emit, "
+                         "cc -std=c99 -O1)" if kind == "reference"
+                         else "the oracle port")
+                      + f" on {threads} thread(s)",
+            "seconds": dt * reps}
+
+# }}}
 
 
-def probe_fp64(dev):
+# {{{ other BASELINE configs (not the driver's line; for the record)
+
+def other_bench(args, local):
+    import numpy as np
     import torch
 
-    from paper_1503_07659_b200 import abi
-    lib = abi.load()
-    out = torch.zeros(148 * 8 * 256, dtype=torch.float64, device=dev)
-    iters = 20000
-    st = torch.cuda.current_stream(dev).cuda_stream
-    lib.lfb_probe_fp64(out.data_ptr(), iters, 148 * 8, 256, st)
-    torch.cuda.synchronize()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e0.record()
-    lib.lfb_probe_fp64(out.data_ptr(), iters, 148 * 8, 256, st)
-    e1.record()
-    torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1)
-    ops = 148 * 8 * 256 * iters * 8 * 2
-    return ops / (ms * 1e-3) / 1e12
+    import paper_1503_07659_b200 as lfb
+    from paper_1503_07659_b200 import fixtures as fx
+    dev = torch.device("cuda", local)
+    peak, peak_src = _peaks()
+    wl = args.workload
+    gen = torch.Generator(device=dev).manual_seed(0)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def run_timed(fn, bytes_, flops=None, flush_l2=True):
+        def step():
+            if flush_l2:
+                flush.fill_(1)  # 256 MB > 126 MB L2
+            fn()
+        # time the kernel alone with events around it, flush outside
+        for _ in range(args.warmup):
+            step()
+        torch.cuda.synchronize()
+        times = []
+        with Clocks(local) as clk:
+            for _ in range(args.steps):
+                if flush_l2:
+                    flush.fill_(1)
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record()
+                fn()
+                e1.record()
+                torch.cuda.synchronize()
+                times.append(e0.elapsed_time(e1))
+        ms = statistics.median(times)
+        out = {"ms_per_step": ms, "ms_best": min(times),
+               "clocks": clk.summary()}
+        if bytes_:
+            out["roofline"] = {"bound": "hbm",
+                               "achieved": bytes_ / (ms * 1e-3) / 1e9,
+                               "peak": peak, "unit": "GB/s",
+                               "frac": bytes_ / (ms * 1e-3) / 1e9 / peak,
+                               "traffic": _traffic(wl),
+                               "peak_source": peak_src}
+        if flops:
+            out["tflops"] = flops / (ms * 1e-3) / 1e12
+        return out
+
+    if wl in ("fill", "axpy"):
+        n = 1 << 24
+        src = fx.fill_source("f64") if wl == "fill" else fx.axpy_source("f64")
+        _r, knl = fx.translate(src)
+        x = torch.rand(n, dtype=torch.float64, device=dev, generator=gen)
+        y = torch.rand(n, dtype=torch.float64, device=dev, generator=gen)
+        bufs = {"out": y} if wl == "fill" else {"y": y, "x": x}
+        env = lfb.env_from_buffers(knl, {"n": n}, bufs,
+                                   {"a": 1.5, "alpha": 1.25})
+        L = lfb.Launcher(knl, env)
+        r = run_timed(L.launch, (8 if wl == "fill" else 24) * n)
+        r.update({"metric": f"{wl} fp64 n=2^24 GB/s", "unit": "GB/s",
+                  "value": r["roofline"]["achieved"]})
+        return r
+    if wl == "matvec":
+        n = 4096
+        _r, knl = fx.translate(fx.matvec_source("f64"))
+        a = torch.rand(n * n, dtype=torch.float64, device=dev, generator=gen)
+        x = torch.rand(n, dtype=torch.float64, device=dev, generator=gen)
+        y = torch.empty(n, dtype=torch.float64, device=dev)
+        env = lfb.env_from_buffers(knl, {"n": n}, {"a": a, "x": x, "y": y})
+        L = lfb.Launcher(knl, env, variant=args.variant)
+        r = run_timed(L.launch, 8 * n * n + 16 * n, 2 * n * n)
+        r.update({"metric": "matvec fp64 4096^2 GB/s", "unit": "GB/s",
+                  "value": r["roofline"]["achieved"]})
+        return r
+    if wl == "sgemm":
+        m = n = l = args.gemm_n
+        _r, knl = fx.translate(fx.gemm_source("f32"))
+        a = torch.rand(m * l, dtype=torch.float32, device=dev, generator=gen)
+        b = torch.rand(l * n, dtype=torch.float32, device=dev, generator=gen)
+        c = torch.rand(m * n, dtype=torch.float32, device=dev, generator=gen)
+        env = lfb.env_from_buffers(knl, {"m": m, "n": n, "l": l},
+                                   {"a": a, "b": b, "c": c}, {"alpha": 1.5})
+        L = lfb.Launcher(knl, env, variant=args.variant)
+        r = run_timed(L.launch, None, 2.0 * m * n * l, flush_l2=False)
+        r.update({"metric": f"sgemm fp32 {m}^3 TFLOP/s", "unit": "TFLOP/s",
+                  "value": r["tflops"], "variant": args.variant})
+        return r
+    if wl == "sweep":
+        rows = []
+        for n in range(4, 17):
+            nelt = (1 << 25) // n ** 3 // 32 * 32
+            _r, knl = fx.translate(fx.semlap_source(n))
+            u, d, g, w = sem_buffers(n, nelt, dev, n)
+            env = lfb.env_from_buffers(knl, {"nelt": nelt},
+                                       {"u": u, "d": d, "g": g, "w": w})
+            L = lfb.Launcher(knl, env)
+            r = run_timed(L.launch, 64 * n ** 3 * nelt, flush_l2=False)
+            rows.append({"order": n - 1, "npts": n, "nelt": nelt,
+                         "ms": r["ms_per_step"],
+                         "gdofs": nelt * n ** 3 / (r["ms_per_step"] * 1e-3)
+                         / 1e9,
+                         "hbm_frac": r["roofline"]["frac"],
+                         "sm_mhz": r["clocks"]["sm_mhz"]})
+            del u, d, g, w, env, L
+            torch.cuda.empty_cache()
+        return {"metric": "SEM sweep orders 3-15 GDOF/s", "rows": rows}
+    raise SystemExit(f"unknown workload {wl}")
+
+# }}}
 
 
 def main():
@@ -393,66 +552,67 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="sem2m")
     ap.add_argument("--variant", type=int, default=0)
+    ap.add_argument("--gemm-n", type=int, default=8192)
     ap.add_argument("--no-verify", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--e2e-nelt", type=int, default=0)
     args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
     args.npts = 8
     args.nelt = {"sem2m": 1 << 21, "sem65k": 65536}.get(args.workload,
                                                          1 << 21)
-    args.warmup = max(args.warmup, 3)
+    threads = os.cpu_count() or 1
 
     if args.impl == "reference":
-        rank = int(os.environ.get("RANK", "0"))
-        if rank != 0:
+        # the reference's own CPU execution of the path, rank 0 only
+        if int(os.environ.get("RANK", "0")) != 0:
             return
-        threads = os.cpu_count() or 1
-        cpu = cpu_reference_rate(args.npts, 65536, threads, min_seconds=5.0)
-        per_step_ms = 1e3 * 65536 * args.npts**3 / (cpu["value"] * 1e9)
-        res = {"metric": METRIC, "value": cpu["value"], "unit": "GDOF/s",
-               "impl": "reference", "n_gpus": args.gpus, "steps": args.steps,
-               "warmup": args.warmup, "ms_per_step": per_step_ms,
+        sample = 65536
+        per_step = []
+        cpu = None
+        for _ in range(args.warmup + args.steps):
+            cpu = cpu_reference(args.npts, sample, threads, 0.0)
+            per_step.append(cpu["value"])
+        value = statistics.median(per_step[args.warmup:])
+        cpu["value"] = value
+        res = {"metric": METRIC, "value": value, "unit": "GDOF/s",
+               "impl": "reference", "n_gpus": args.gpus,
+               "steps": args.steps, "warmup": args.warmup,
+               "ms_per_step": 1e3 * args.nelt * args.npts ** 3
+               / (value * 1e9),
                "higher_is_better": True, "scaling": "strong",
                "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-               "config": {"workload": f"semlap order 7 fp64, "
-                                      f"{args.nelt} elements (timed on a "
-                                      "65,536-element sample)",
+               "config": {"workload": f"semlap order {args.npts - 1} "
+                                      f"(n={args.npts}) fp64, {args.nelt} "
+                                      "elements; each step times a "
+                                      f"{sample}-element sample",
                           "nelt": args.nelt, "npts": args.npts},
                "cpu_baseline": cpu,
-               "e2e": {"value": cpu["value"], "unit": "GDOF/s",
+               "e2e": {"value": value, "unit": "GDOF/s",
                        "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(res))
         return
 
     rank, world, local = dist_init(args.gpus)
     import torch
-    res, launcher, env, bufs, knl = sem_workload(args, rank, world, local)
+    if args.workload not in ("sem2m", "sem65k"):
+        if rank == 0:
+            print(json.dumps(other_bench(args, local)))
+        return
+    res, knl = sem_bench(args, rank, world, local)
     dev = torch.device("cuda", local)
-    res["clocks"] = None
-    # clocks from the timed region were captured inside sem_workload? keep
-    # a separate short sampled re-run so the numbers come with a record
-    with Clocks(local) as clk:
-        st = torch.cuda.current_stream(dev)
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(st)
-        for _ in range(args.steps):
-            launcher.launch()
-        e1.record(st)
-        torch.cuda.synchronize()
-    res["clocks"] = clk.summary()
-    res["fp64_probe_tflops"] = probe_fp64(dev)
-    del bufs, env, launcher
-    torch.cuda.empty_cache()
-    if rank == 0 and world == 1 and not args.no_e2e:
-        res["e2e"] = sem_e2e(args, knl, args.npts, 65536, dev)
-    else:
-        res["e2e"] = None
+    res["e2e"] = None
+    if not args.no_e2e:
+        nelt_e2e = args.e2e_nelt or (args.nelt // world)
+        e2e = sem_e2e(knl, args.npts, nelt_e2e, dev, steps=3)
+        ms = max_over_ranks(e2e["ms_per_step"], world)
+        e2e["value"] = nelt_e2e * world * args.npts ** 3 / (ms * 1e-3) / 1e9
+        e2e["ms_per_step"] = ms
+        res["e2e"] = e2e
+    res["cpu_baseline"] = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        threads = os.cpu_count() or 1
-        res["cpu_baseline"] = cpu_reference_rate(args.npts, 65536, threads)
-    else:
-        res["cpu_baseline"] = None
+        res["cpu_baseline"] = cpu_reference(args.npts, 65536, threads, 15.0)
     res.update({"n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "higher_is_better": True,
                 "vs_baseline": None, "data": "synthetic"})

@@ -123,6 +123,10 @@ int lfb_sgemm_f32(float alpha, const float *a, const float *b, float *c,
  * kernel runs against: iters x 8 independent DMUL+DADD chains per thread. */
 int lfb_probe_fp64(double *out, int iters, int blocks, int threads,
                    lfb_stream stream);
+/* The SEM kernel's HBM access mix without its arithmetic (read u + 6 g,
+ * write w per point): the streaming ceiling at a given footprint. */
+int lfb_probe_stream(double *w, const double *u, const double *g,
+                     int64_t npoints, lfb_stream stream);
 
 #ifdef __cplusplus
 }

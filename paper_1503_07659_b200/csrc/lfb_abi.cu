@@ -54,9 +54,40 @@ __global__ void probe_fp64_kernel(double *out, int iters) {
   if (s == 123.456) out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 
+// The SEM kernel's HBM traffic without its arithmetic: per point read u (8 B)
+// and the 6 g values (48 B), write w (8 B) -- the ceiling of that access mix
+// at a given footprint (bench.py reports it beside the roofline).
+__global__ void probe_stream_kernel(double *__restrict__ w,
+                                    const double *__restrict__ u,
+                                    const double *__restrict__ g,
+                                    int64_t npoints) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+       2 * p + 1 < npoints; p += stride) {
+    const double2 uv = __ldcs(reinterpret_cast<const double2 *>(u) + p);
+    const double2 *gp = reinterpret_cast<const double2 *>(g) + 6 * p;
+    double2 a = __ldcs(gp), b = __ldcs(gp + 1), c = __ldcs(gp + 2);
+    double2 d = __ldcs(gp + 3), e = __ldcs(gp + 4), f = __ldcs(gp + 5);
+    double2 r;
+    r.x = uv.x + a.x + b.y + d.x;
+    r.y = uv.y + c.x + e.y + f.x;
+    __stcs(reinterpret_cast<double2 *>(w) + p, r);
+  }
+}
+
 }  // namespace lfb
 
 extern "C" {
+
+int lfb_probe_stream(double *w, const double *u, const double *g,
+                     int64_t npoints, lfb_stream stream) {
+  if (!w || !u || !g || npoints < 2)
+    return lfb::fail(LFB_ERR_ARG, "lfb_probe_stream: bad arguments");
+  int sms = lfb::sm_count(nullptr);
+  lfb::probe_stream_kernel<<<sms * 8, 256, 0, (cudaStream_t)stream>>>(
+      w, u, g, npoints);
+  return lfb::check_launch("lfb_probe_stream");
+}
 
 int lfb_abi_version(void) { return LFB_ABI_VERSION; }
 

@@ -1,0 +1,34 @@
+// Pieces shared by the two SEM kernels: the fused verification-norm epilogue.
+#pragma once
+
+#include "lfb_common.cuh"
+
+namespace lfb {
+
+// fixed-order block reduction of a per-thread sum(w*w) -> partials[blockIdx]
+// (deterministic: warp shuffles in a fixed pattern, warps in index order)
+__device__ __forceinline__ void block_sumsq_partial(double acc,
+                                                    double *partials) {
+  __shared__ double red[32];
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1)
+    acc = dadd(acc, __shfl_down_sync(0xffffffffu, acc, off));
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double sum = 0.0;
+    for (int q = 0; q < (int)(blockDim.x / 32); ++q) sum = dadd(sum, red[q]);
+    partials[blockIdx.x] = sum;
+  }
+}
+
+// partials[0..n) -> *out in index order (one thread; n ~ #SMs)
+int sem_sumsq_finish(const double *partials, int n, double *out,
+                     cudaStream_t s);
+
+int sem_slab_dispatch(int n, double *w, const double *u, const double *d,
+                      const double *g, int64_t nelt, const lfb_launch *geom,
+                      cudaStream_t s, int64_t *grid_out);
+
+}  // namespace lfb

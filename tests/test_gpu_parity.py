@@ -101,17 +101,28 @@ def test_semlap_o7_65536_elements(cuda):
                [(0, 1024), (30000, 31000), (nelt - 1024, nelt)])
 
 
-@pytest.mark.parametrize("variant", [1, 2, 3])
+@pytest.mark.parametrize("variant", [1, 2, 3, 4, 5, 6, 7, 9, 10, 11, 12, 13, 14, 15, 16, 17, 18, 19])
 def test_semlap_o7_variants(cuda, variant):
     nelt = 4096
     _sem_check(8, nelt, fx.semlap_source(8), cuda, [(0, nelt)],
                variant=variant)
 
 
-@pytest.mark.parametrize("n", [2, 4, 6, 8, 10])
+@pytest.mark.parametrize("n", list(range(2, 17)))
 def test_semlap_orders(cuda, n):
-    nelt = 640
+    """The order sweep of BASELINE config 5 (p = 1..15): staged kernel for
+    even n <= 10, k-slab kernel for odd n and n >= 12."""
+    nelt = 640 if n <= 10 else 96
     _sem_check(n, nelt, fx.semlap_source(n), cuda, [(0, nelt)], seed=n)
+
+
+@pytest.mark.parametrize("n,nelt", [(5, 3), (7, 1), (9, 37), (15, 5),
+                                    (3, 101)])
+def test_semlap_odd_order_tail(cuda, n, nelt):
+    """Odd n and odd nelt: the last element's 16-byte-rounded u copy would
+    run past the array, so the threads copy it themselves."""
+    src = fx.semlap_source(n, block=1)
+    _sem_check(n, nelt, src, cuda, [(0, nelt)], seed=nelt)
 
 
 @pytest.mark.parametrize("block,nelt", [(1, 37), (7, 100), (32, 33),
@@ -123,11 +134,10 @@ def test_semlap_ragged_and_guarded(cuda, block, nelt):
     _sem_check(8, nelt, src, cuda, [(0, nelt)], seed=block)
 
 
-def test_semlap_sumsq_epilogue(cuda):
-    n, nelt = 8, 3000
+@pytest.mark.parametrize("n", [8, 5])
+def test_semlap_sumsq_epilogue(cuda, n):
     _raw, knl = fx.translate(fx.semlap_source(n))
-    # nelt must satisfy the fixture's assume(nelt mod 32 = 0)
-    nelt = 3008
+    nelt = 3008  # the fixture assumes nelt mod 32 = 0
     u, d, g = _sem_inputs(n, nelt, cuda, 5)
     w = torch.empty_like(u)
     env = lfb.env_from_buffers(knl, {"nelt": nelt},
