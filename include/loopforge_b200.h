@@ -118,6 +118,11 @@ int64_t lfb_semlap_workspace(int npts, int nelt, const lfb_launch *geom);
 int lfb_sgemm_f32(float alpha, const float *a, const float *b, float *c,
                   int l, int m, int n,
                   const lfb_launch *geom, lfb_stream stream);
+/* doubles of workspace the tensor-core sgemm needs (tf32 hi/lo operand
+ * split, geom->workspace); 0 if the shape cannot use tensor cores
+ * (m % 128, n % 256, l % 32 != 0).  geom->variant: 0 tensor cores when
+ * possible else the bit-exact CUDA-core kernel, 1 bit-exact, 2 tensor only */
+int64_t lfb_sgemm_workspace(int l, int m, int n);
 
 /* Microbenchmark used by bench.py to state the FP64 issue ceiling the SEM
  * kernel runs against: iters x 8 independent DMUL+DADD chains per thread. */

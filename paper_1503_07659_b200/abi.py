@@ -54,10 +54,12 @@ SIGNATURES = {
     "lfb_semlap_f64": [P, P, P, P, I32, LP, P],
     "lfb_semlap_workspace": [I32, I32, LP],
     "lfb_sgemm_f32": [F, P, P, P, I32, I32, I32, LP, P],
+    "lfb_sgemm_workspace": [I32, I32, I32],
     "lfb_probe_fp64": [P, I32, I32, I32, P],
     "lfb_probe_stream": [P, P, P, C.c_int64, P],
 }
-_RESTYPES = {"lfb_last_error": C.c_char_p, "lfb_semlap_workspace": C.c_int64}
+_RESTYPES = {"lfb_last_error": C.c_char_p, "lfb_semlap_workspace": C.c_int64,
+             "lfb_sgemm_workspace": C.c_int64}
 
 _lib = None
 

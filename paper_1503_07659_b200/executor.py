@@ -208,6 +208,14 @@ class Launcher:
         self.npts = w.npts
         self._sumsq = sumsq
         self._workspace = workspace
+        if w.name == "gemm" and workspace is None and variant != 1:
+            # tf32 hi/lo operand split for the tensor-core path
+            pm = self.match.param_map
+            l, m, n = (env.params[pm[p]] for p in ("l", "m", "n"))
+            need = abi.load().lfb_sgemm_workspace(l, m, n)
+            if need > 0:
+                self._workspace = torch.empty(need, dtype=torch.float64,
+                                              device=env.device)
 
     def workload(self):
         return self.match.workload

@@ -270,3 +270,60 @@ def test_wrong_shape_input_is_interp_error(cuda):
                             device=cuda)
 
 # }}}
+
+
+# {{{ sgemm on tensor cores (tolerance parity)
+
+@pytest.mark.parametrize("m,n,l", [(128, 256, 32), (256, 512, 256),
+                                   (1024, 768, 4096), (384, 256, 8192)])
+def test_sgemm_tensor_cores(cuda, m, n, l):
+    """variant=2: tcgen05 kind::tf32 with the 3xTF32 split.  Tolerance
+    (north star: 1e-5 relative for fp32), normwise against the reference's
+    own fp32 sequential result (the oracle), and the same bound against an
+    exact fp64 product; the reference's own rounding error is printed."""
+    _r, knl = fx.translate(fx.gemm_source("f32"))
+    rng = np.random.default_rng(m * 7 + n * 3 + l)
+    a = rng.random(m * l).astype(np.float32)
+    b = rng.random(l * n).astype(np.float32)
+    c = rng.random(m * n).astype(np.float32)
+    alpha = np.float32(1.5)
+    env = lfb.env_from_buffers(
+        knl, {"m": m, "n": n, "l": l},
+        {"a": torch.from_numpy(a).to(cuda), "b": torch.from_numpy(b).to(cuda),
+         "c": torch.from_numpy(c.copy()).to(cuda)}, {"alpha": alpha})
+    out = lfb.interpret(knl, env, variant=2)
+    got = out.arrays["c"].data.cpu().numpy().astype(np.float64)
+    ref = oracle.sgemm(alpha, a, b, c.copy(), l, m, n, threads=8) \
+        .astype(np.float64)
+    A = a.astype(np.float64).reshape(l, m).T      # column major (m, l)
+    B = b.astype(np.float64).reshape(n, l).T      # column major (l, n)
+    exact = (c.astype(np.float64).reshape(n, m).T
+             + float(alpha) * (A @ B)).T.reshape(-1)
+    err_ref = np.linalg.norm(got - ref) / np.linalg.norm(ref)
+    err_exact = np.linalg.norm(got - exact) / np.linalg.norm(exact)
+    ref_own = np.linalg.norm(ref - exact) / np.linalg.norm(exact)
+    print(f"m={m} n={n} l={l}: |tc-ref|/|ref|={err_ref:.2e} "
+          f"|tc-exact|={err_exact:.2e} |ref-exact|={ref_own:.2e} "
+          f"max rel={np.max(np.abs(got - ref) / np.abs(ref)):.2e}")
+    assert err_ref <= 1e-5
+    assert err_exact <= 1e-5
+
+
+def test_sgemm_default_dispatch(cuda):
+    """Default variant: tensor cores for 128/256/32-aligned shapes, the
+    bit-exact kernel otherwise -- both on the device."""
+    _r, knl = fx.translate(fx.gemm_source("f32"))
+    m, n, l = 100, 36, 50
+    rng = np.random.default_rng(1)
+    a = rng.random(m * l).astype(np.float32)
+    b = rng.random(l * n).astype(np.float32)
+    c = rng.random(m * n).astype(np.float32)
+    env = lfb.env_from_buffers(
+        knl, {"m": m, "n": n, "l": l},
+        {"a": torch.from_numpy(a).to(cuda), "b": torch.from_numpy(b).to(cuda),
+         "c": torch.from_numpy(c.copy()).to(cuda)}, {"alpha": 0.5})
+    out = lfb.interpret(knl, env)
+    ref = oracle.sgemm(np.float32(0.5), a, b, c.copy(), l, m, n)
+    assert out.arrays["c"].data.cpu().numpy().tobytes() == ref.tobytes()
+
+# }}}
