@@ -605,6 +605,15 @@ def main():
     res["e2e"] = None
     if not args.no_e2e:
         nelt_e2e = args.e2e_nelt or (args.nelt // world)
+        # pinned host buffers hold u, g, w (72 B/dof): stay within a third
+        # of the host's available memory (shared by all local ranks)
+        try:
+            import psutil
+            avail = psutil.virtual_memory().available
+            cap = avail // 3 // max(1, world) // (72 * args.npts ** 3)
+            nelt_e2e = max(32, min(nelt_e2e, cap // 32 * 32))
+        except Exception:
+            pass
         e2e = sem_e2e(knl, args.npts, nelt_e2e, dev, steps=3)
         ms = max_over_ranks(e2e["ms_per_step"], world)
         e2e["value"] = nelt_e2e * world * args.npts ** 3 / (ms * 1e-3) / 1e9

@@ -127,7 +127,12 @@ def summarise(rep, key, rnd):
         lines.append("")
         rd = _bytes(*m.get("dram__bytes_read.sum", ("", "")))
         wr = _bytes(*m.get("dram__bytes_write.sum", ("", "")))
-        dur = _num(m.get("gpu__time_duration.sum", ("", ""))[0])
+        dv, du = m.get("gpu__time_duration.sum", ("", ""))
+        dur = _num(dv)
+        if dur is not None:
+            dur *= {"ns": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3,
+                    "msecond": 1e3, "s": 1e6, "second": 1e6}.get(
+                        du.strip(), 1.0)
         if idx == 0:
             summary = {"dram_bytes_per_launch": (rd or 0) + (wr or 0),
                        "dram_read_bytes": rd, "dram_write_bytes": wr,
