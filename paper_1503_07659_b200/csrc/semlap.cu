@@ -608,11 +608,14 @@ static int sem_dispatch(double *w, const double *u, const double *d,
   LFB_SEM_TABLE(S, A)
 #undef S
 #undef A
-  // odd n, n >= 12, or variant 9: the k-slab streaming kernel
-  if (var == 0 || var == 9)
-    return sem_slab_dispatch(n, w, u, d, g, nelt, geom, s, grid_out);
-  return fail(LFB_ERR_UNSUPPORTED,
-              "semlap: no sm_100a kernel variant %d for n=%d", var, n);
+  // other orders: whole-chunk staging (n <= 11), else / variant 9 the k-slab
+  // streaming kernel
+  if (var == 0 || var >= 20) {
+    const int rc = sem_gen_dispatch(n, var, w, u, d, g, nelt, geom, s,
+                                    grid_out);
+    if (rc != -1) return rc;
+  }
+  return sem_slab_dispatch(n, var, w, u, d, g, nelt, geom, s, grid_out);
 }
 
 // }}}

@@ -27,7 +27,13 @@ __device__ __forceinline__ void block_sumsq_partial(double acc,
 int sem_sumsq_finish(const double *partials, int n, double *out,
                      cudaStream_t s);
 
-int sem_slab_dispatch(int n, double *w, const double *u, const double *d,
+// -1 when the general kernel has no entry for (n, variant)
+int sem_gen_dispatch(int n, int variant, double *w, const double *u,
+                     const double *d, const double *g, int64_t nelt,
+                     const lfb_launch *geom, cudaStream_t s,
+                     int64_t *grid_out);
+
+int sem_slab_dispatch(int n, int variant, double *w, const double *u, const double *d,
                       const double *g, int64_t nelt, const lfb_launch *geom,
                       cudaStream_t s, int64_t *grid_out);
 

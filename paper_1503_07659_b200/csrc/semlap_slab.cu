@@ -34,27 +34,33 @@ struct SlabCfg {
   static constexpr int SLAB = 6 * N2;
 };
 
-template <int N, int G, int SGS>
+template <int N, int G, int SGS, int KS>
 struct SlabSmem {
   using C = SlabCfg<N>;
   static constexpr size_t bars = 256;  // G * (2 + SGS) <= 32 mbarriers
   static constexpr size_t d_off = bars;
   static constexpr size_t grp_off = (d_off + 2 * N * N * 8 + 127) / 128 * 128;
   static constexpr size_t grp_bytes =
-      ((2 * (size_t)C::UST + (size_t)SGS * C::SLAB + 2 * (size_t)C::SCR) * 8 +
+      ((2 * (size_t)C::UST + (size_t)SGS * KS * C::SLAB + 2 * (size_t)C::SCR) *
+           8 +
        127) / 128 * 128;
   static constexpr size_t total = grp_off + G * grp_bytes;
 };
 
-template <int N, int G, int SGS, bool SUMSQ>
+// KS consecutive k-slices of g per bulk copy (one ring slot), N / KS copies
+// per element (the last one shorter when KS does not divide N).  Both phases
+// are fully unrolled over k and l, so the n independent accumulation chains
+// of a thread's column overlap in the FP64 pipe.
+template <int N, int G, int SGS, int KS, bool DREG, bool SUMSQ>
 __global__ void __launch_bounds__(G *SlabCfg<N>::T, 1)
     semlap_slab_kernel(double *__restrict__ w, const double *__restrict__ u,
                        const double *__restrict__ d,
                        const double *__restrict__ g, int64_t nelt,
                        double *__restrict__ partials) {
   using C = SlabCfg<N>;
-  using L = SlabSmem<N, G, SGS>;
+  using L = SlabSmem<N, G, SGS, KS>;
   constexpr int NP = C::NP, N2 = C::N2, T = C::T, R = C::R;
+  constexpr int STEPS = (N + KS - 1) / KS;  // slab copies per element
   static_assert(G * (2 + SGS) <= 32, "too many mbarriers");
 
   extern __shared__ __align__(128) unsigned char smem[];
@@ -71,17 +77,17 @@ __global__ void __launch_bounds__(G *SlabCfg<N>::T, 1)
 
   unsigned char *gbase = smem + L::grp_off + (size_t)grp * L::grp_bytes;
   double *ustage = reinterpret_cast<double *>(gbase);      // 2 x UST
-  double *slabs = ustage + 2 * C::UST;                     // SGS x SLAB
-  double *scr_r = slabs + SGS * C::SLAB;                   // SCR
+  double *slabs = ustage + 2 * C::UST;                     // SGS x KS x SLAB
+  double *scr_r = slabs + SGS * KS * C::SLAB;              // SCR
   double *scr_s = scr_r + C::SCR;                          // SCR
   uint64_t *ubar = bars + grp * (2 + SGS);
   uint64_t *gbar = ubar + 2;
 
-  const int64_t begin = (nelt * blockIdx.x) / gridDim.x;
-  const int64_t end = (nelt * (blockIdx.x + 1)) / gridDim.x;
-  const int64_t count = end - begin;
-  // group grp handles CTA-local elements grp, grp + G, ...
-  const int64_t mine = count > grp ? (count - grp + G - 1) / G : 0;
+  // interleaved: group q0 = blockIdx.x * G + grp takes elements q0, q0 + Q..
+  const int64_t q0 = (int64_t)blockIdx.x * G + grp;
+  const int64_t Q = (int64_t)gridDim.x * G;
+  const int64_t mine = nelt > q0 ? (nelt - q0 + Q - 1) / Q : 0;
+  auto elem = [&](int64_t m) -> int64_t { return q0 + m * Q; };
 
   if (tid == 0) {
     for (int q = 0; q < G * (2 + SGS); ++q) mbar_init(&bars[q], 1);
@@ -101,7 +107,7 @@ __global__ void __launch_bounds__(G *SlabCfg<N>::T, 1)
     return (e * NP - u_lead(e)) * 8 + u_span(e) <= u_bytes_total;
   };
   auto issue_u = [&](int64_t m) {
-    const int64_t e = begin + grp + m * G;
+    const int64_t e = elem(m);
     const int st = (int)(m & 1);
     if (u_bulk_ok(e)) {
       mbar_arrive_expect_tx(&ubar[st], (uint32_t)u_span(e));
@@ -111,20 +117,23 @@ __global__ void __launch_bounds__(G *SlabCfg<N>::T, 1)
       mbar_arrive_expect_tx(&ubar[st], 0);  // threads copy it themselves
     }
   };
-  auto issue_slab = [&](int64_t q) {  // q = m * N + k
-    const int64_t m = q / N;
-    const int k = (int)(q % N);
-    const int64_t e = begin + grp + m * G;
+  auto issue_slab = [&](int64_t q) {  // q = m * STEPS + step
+    const int64_t m = q / STEPS;
+    const int step = (int)(q % STEPS);
+    const int k0 = step * KS;
+    const int nk = (N - k0) < KS ? (N - k0) : KS;
+    const int64_t e = elem(m);
     const int slot = (int)(q % SGS);
-    mbar_arrive_expect_tx(&gbar[slot], (uint32_t)(C::SLAB * 8));
-    bulk_g2s_stream(slabs + (size_t)slot * C::SLAB,
-                    g + e * 6 * NP + (int64_t)k * 6 * N2, C::SLAB * 8,
+    mbar_arrive_expect_tx(&gbar[slot], (uint32_t)(nk * C::SLAB * 8));
+    bulk_g2s_stream(slabs + (size_t)slot * KS * C::SLAB,
+                    g + e * 6 * NP + (int64_t)k0 * 6 * N2, nk * C::SLAB * 8,
                     &gbar[slot], pol);
   };
 
+  const int64_t nsteps = mine * STEPS;
   if (lt == 0) {
     for (int64_t m = 0; m < 2 && m < mine; ++m) issue_u(m);
-    for (int64_t q = 0; q < SGS && q < mine * N; ++q) issue_slab(q);
+    for (int64_t q = 0; q < SGS && q < nsteps; ++q) issue_slab(q);
   }
   for (int q = tid; q < N2; q += G * T) {
     const double v = d[q];
@@ -135,7 +144,7 @@ __global__ void __launch_bounds__(G *SlabCfg<N>::T, 1)
 
   double acc = 0.0;
   for (int64_t m = 0; m < mine; ++m) {
-    const int64_t e = begin + grp + m * G;
+    const int64_t e = elem(m);
     const int st = (int)(m & 1);
     mbar_wait(&ubar[st], (uint32_t)((m >> 1) & 1));
     const double *su = ustage + st * C::UST + u_lead(e);
@@ -147,45 +156,58 @@ __global__ void __launch_bounds__(G *SlabCfg<N>::T, 1)
 
     double wt[N];
     double ucol[N];
+    double da[N], db[N];  // d(i,.), d(j,.) (DREG)
     if (active) {
 #pragma unroll
       for (int l = 0; l < N; ++l) ucol[l] = su[i + N * j + N2 * l];
+      if constexpr (DREG) {
+#pragma unroll
+        for (int l = 0; l < N; ++l) da[l] = dn[i + N * l], db[l] = dn[j + N * l];
+      }
     }
-#pragma unroll 1
-    for (int k = 0; k < N; ++k) {
-      const int64_t q = m * N + k;
+#pragma unroll
+    for (int step = 0; step < STEPS; ++step) {
+      const int64_t q = m * STEPS + step;
       const int slot = (int)(q % SGS);
       mbar_wait(&gbar[slot], (uint32_t)((q / SGS) & 1));
       if (active) {
-        double ur = 0.0, us = 0.0, ut = 0.0;
-        const double *row = su + N * j + N2 * k;
-        const double *col = su + i + N2 * k;
-        const double *dk = dt + N * k;
+        const double *gs = slabs + (size_t)slot * KS * C::SLAB;
 #pragma unroll
-        for (int l = 0; l < N; ++l) {
-          ur = dadd(ur, dmul(dn[i + N * l], row[l]));
-          us = dadd(us, dmul(dn[j + N * l], col[N * l]));
-          ut = dadd(ut, dmul(dk[l], ucol[l]));
+        for (int kk = 0; kk < KS; ++kk) {
+          const int k = step * KS + kk;
+          if (k < N) {
+            double ur = 0.0, us = 0.0, ut = 0.0;
+            const double *row = su + N * j + N2 * k;
+            const double *col = su + i + N2 * k;
+            const double *dk = dt + N * k;  // d(k, .)
+#pragma unroll
+            for (int l = 0; l < N; ++l) {
+              const double a = DREG ? da[l] : dn[i + N * l];
+              const double b = DREG ? db[l] : dn[j + N * l];
+              ur = dadd(ur, dmul(a, row[l]));
+              us = dadd(us, dmul(b, col[N * l]));
+              ut = dadd(ut, dmul(dk[l], ucol[l]));
+            }
+            const double *gp = gs + kk * C::SLAB + 6 * (i + N * j);
+            const double2 g01 = *reinterpret_cast<const double2 *>(gp);
+            const double2 g23 = *reinterpret_cast<const double2 *>(gp + 2);
+            const double2 g45 = *reinterpret_cast<const double2 *>(gp + 4);
+            scr_r[i + R * j + R * N * k] =
+                dadd(dadd(dmul(g01.x, ur), dmul(g01.y, us)), dmul(g23.x, ut));
+            scr_s[i + R * j + R * N * k] =
+                dadd(dadd(dmul(g01.y, ur), dmul(g23.y, us)), dmul(g45.x, ut));
+            wt[k] =
+                dadd(dadd(dmul(g23.x, ur), dmul(g45.x, us)), dmul(g45.y, ut));
+          }
         }
-        const double *gp = slabs + (size_t)slot * C::SLAB + 6 * (i + N * j);
-        const double g0 = gp[0], g1 = gp[1], g2 = gp[2], g3 = gp[3],
-                     g4 = gp[4], g5 = gp[5];
-        scr_r[i + R * j + R * N * k] =
-            dadd(dadd(dmul(g0, ur), dmul(g1, us)), dmul(g2, ut));
-        scr_s[i + R * j + R * N * k] =
-            dadd(dadd(dmul(g1, ur), dmul(g3, us)), dmul(g4, ut));
-        const double wtk = dadd(dadd(dmul(g2, ur), dmul(g4, us)), dmul(g5, ut));
-#pragma unroll
-        for (int kk = 0; kk < N; ++kk)
-          if (kk == k) wt[kk] = wtk;
       }
-      named_bar_sync(1 + grp, T);  // slab consumed (and, at k = N-1, u)
+      named_bar_sync(1 + grp, T);  // slot consumed (and, last step, u)
       if (lt == 0) {
-        if (q + SGS < mine * N) {
+        if (q + SGS < nsteps) {
           fence_proxy_async_smem();
           issue_slab(q + SGS);
         }
-        if (k == N - 1 && m + 2 < mine) {
+        if (step == STEPS - 1 && m + 2 < mine) {
           fence_proxy_async_smem();
           issue_u(m + 2);
         }
@@ -193,22 +215,23 @@ __global__ void __launch_bounds__(G *SlabCfg<N>::T, 1)
     }
 
     if (active) {
+      if constexpr (DREG) {
+#pragma unroll
+        for (int l = 0; l < N; ++l) da[l] = dt[i + N * l], db[l] = dt[j + N * l];
+      }
       double *we = w + e * NP + i + N * j;
-#pragma unroll 1
+#pragma unroll
       for (int k = 0; k < N; ++k) {
         double s = 0.0;
-        const double *rr = scr_r + R * j + R * N * k;
-        const double *rs = scr_s + i + R * N * k;
-        const double *dk = dn + N * k;
+        const double *rr = scr_r + R * j + R * N * k;  // wr(., j, k)
+        const double *rs = scr_s + i + R * N * k;      // ws(i, ., k)
+        const double *dk = dn + N * k;                 // d(., k)
 #pragma unroll
         for (int l = 0; l < N; ++l) {
-          double wtl = 0.0;
-#pragma unroll
-          for (int kk = 0; kk < N; ++kk)
-            if (kk == l) wtl = wt[kk];
-          s = dadd(dadd(dadd(s, dmul(dn[l + N * i], rr[l])),
-                        dmul(dn[l + N * j], rs[R * l])),
-                   dmul(dk[l], wtl));
+          const double a = DREG ? da[l] : dt[i + N * l];
+          const double b = DREG ? db[l] : dt[j + N * l];
+          s = dadd(dadd(dadd(s, dmul(a, rr[l])), dmul(b, rs[R * l])),
+                   dmul(dk[l], wt[l]));
         }
         we[N2 * k] = s;
         if constexpr (SUMSQ) acc = dadd(acc, dmul(s, s));
@@ -220,11 +243,11 @@ __global__ void __launch_bounds__(G *SlabCfg<N>::T, 1)
   if constexpr (SUMSQ) block_sumsq_partial(acc, partials);
 }
 
-template <int N, int G, int SGS>
+template <int N, int G, int SGS, int KS, bool DREG>
 int launch_sem_slab(double *w, const double *u, const double *d,
                     const double *g, int64_t nelt, const lfb_launch *geom,
                     cudaStream_t s, int64_t *grid_out) {
-  using L = SlabSmem<N, G, SGS>;
+  using L = SlabSmem<N, G, SGS, KS>;
   static_assert(L::total <= 227 * 1024, "smem");
   const int block = G * SlabCfg<N>::T;
   int sms = sm_count(geom);
@@ -241,49 +264,59 @@ int launch_sem_slab(double *w, const double *u, const double *d,
   const bool sumsq = geom && geom->sumsq;
   if (sumsq && (!geom->workspace || geom->workspace_len < grid))
     return fail(LFB_ERR_ARG, "semlap: sumsq workspace too small");
-  if (sumsq) {
-    auto k = semlap_slab_kernel<N, G, SGS, true>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)L::total);
-    k<<<grid, block, L::total, s>>>(w, u, d, g, nelt, geom->workspace);
-    if (int rc = check_launch("lfb_semlap_f64")) return rc;
-    return sem_sumsq_finish(geom->workspace, grid, geom->sumsq, s);
-  }
-  auto k = semlap_slab_kernel<N, G, SGS, false>;
+  auto k = sumsq ? semlap_slab_kernel<N, G, SGS, KS, DREG, true>
+                 : semlap_slab_kernel<N, G, SGS, KS, DREG, false>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)L::total);
-  k<<<grid, block, L::total, s>>>(w, u, d, g, nelt, nullptr);
-  return check_launch("lfb_semlap_f64");
+  k<<<grid, block, L::total, s>>>(w, u, d, g, nelt,
+                                  sumsq ? geom->workspace : nullptr);
+  if (int rc = check_launch("lfb_semlap_f64")) return rc;
+  return sumsq ? sem_sumsq_finish(geom->workspace, grid, geom->sumsq, s)
+               : LFB_OK;
 }
 
-// n -> (groups per CTA, slab ring depth) that fit 227 KB
-int sem_slab_dispatch(int n, double *w, const double *u, const double *d,
-                      const double *g, int64_t nelt, const lfb_launch *geom,
-                      cudaStream_t s, int64_t *grid_out) {
-  switch (n) {
-#define LFB_SLAB(NN, GG, SS)                                              \
-  case NN:                                                                \
-    return launch_sem_slab<NN, GG, SS>(w, u, d, g, nelt, geom, s, grid_out);
-    LFB_SLAB(2, 4, 4)
-    LFB_SLAB(3, 4, 4)
-    LFB_SLAB(4, 4, 4)
-    LFB_SLAB(5, 4, 4)
-    LFB_SLAB(6, 4, 4)
-    LFB_SLAB(7, 3, 4)
-    LFB_SLAB(8, 3, 4)
-    LFB_SLAB(9, 4, 4)
-    LFB_SLAB(10, 4, 4)
-    LFB_SLAB(11, 3, 4)
-    LFB_SLAB(12, 2, 4)
-    LFB_SLAB(13, 2, 4)
-    LFB_SLAB(14, 1, 4)
-    LFB_SLAB(15, 1, 4)
-    LFB_SLAB(16, 1, 3)
-#undef LFB_SLAB
-    default:
-      return fail(LFB_ERR_UNSUPPORTED,
-                  "semlap: n=%d points per direction outside 2..16", n);
-  }
+// (n, variant) -> (groups per CTA, ring depth, slices per copy, d in regs)
+// variant 0 / 9: default; 30..: tuning alternatives (n >= 12)
+#define LFB_SLAB_TABLE(X)       \
+  X(2, 0, 4, 4, 1, false)       \
+  X(3, 0, 4, 4, 1, false)       \
+  X(4, 0, 4, 4, 1, false)       \
+  X(5, 0, 4, 4, 1, false)       \
+  X(6, 0, 4, 4, 1, false)       \
+  X(7, 0, 3, 4, 1, false)       \
+  X(8, 0, 3, 4, 1, false)       \
+  X(9, 0, 4, 4, 1, false)       \
+  X(10, 0, 4, 4, 1, false)      \
+  X(11, 0, 3, 4, 1, false)      \
+  X(12, 0, 2, 4, 2, true)       \
+  X(12, 30, 2, 4, 1, false)     \
+  X(12, 31, 3, 2, 1, false)     \
+  X(13, 0, 2, 4, 1, false)      \
+  X(13, 31, 2, 4, 1, true)      \
+  X(14, 0, 1, 4, 2, true)       \
+  X(14, 30, 1, 4, 1, false)     \
+  X(14, 31, 1, 3, 2, false)     \
+  X(15, 0, 1, 3, 2, false)      \
+  X(15, 30, 1, 4, 1, false)     \
+  X(16, 0, 1, 3, 2, false)      \
+  X(16, 30, 1, 3, 1, false)     \
+  X(16, 31, 1, 2, 3, false)
+
+int sem_slab_dispatch(int n, int variant, double *w, const double *u,
+                      const double *d, const double *g, int64_t nelt,
+                      const lfb_launch *geom, cudaStream_t s,
+                      int64_t *grid_out) {
+  const int v = variant == 9 ? 0 : variant;
+#define X(NN, VV, GG, SS, KK, DR)                                         \
+  if (n == NN && v == VV)                                                 \
+    return launch_sem_slab<NN, GG, SS, KK, DR>(w, u, d, g, nelt, geom, s, \
+                                               grid_out);
+  LFB_SLAB_TABLE(X)
+#undef X
+  return fail(LFB_ERR_UNSUPPORTED,
+              "semlap: no sm_100a kernel variant %d for n=%d points per "
+              "direction (supported n = 2..16)",
+              variant, n);
 }
 
 }  // namespace lfb

@@ -116,8 +116,44 @@ def test_semlap_orders(cuda, n):
     _sem_check(n, nelt, fx.semlap_source(n), cuda, [(0, nelt)], seed=n)
 
 
+GEN_VARIANTS = [(4, 20), (4, 21), (4, 22), (5, 20), (5, 21), (5, 22),
+                (6, 20), (6, 21), (6, 22), (7, 20), (7, 21), (7, 22),
+                (8, 20), (8, 21), (8, 22), (9, 20), (9, 21), (10, 20),
+                (10, 21), (11, 20)]
+
+
+@pytest.mark.parametrize("n,variant", GEN_VARIANTS)
+def test_semlap_gen_variants(cuda, n, variant):
+    """The E-element-chunk kernel (semlap_gen.cu) in every tabulated
+    configuration; nelt leaves a partial last chunk and, for odd n, a last
+    u span that must be copied by the threads."""
+    nelt = 331
+    _sem_check(n, nelt, fx.semlap_source(n, block=1), cuda, [(0, nelt)],
+               variant=variant, seed=variant + n)
+
+
+SLAB_VARIANTS = [(12, 30), (12, 31), (13, 31), (14, 30), (14, 31),
+                 (15, 30), (16, 30), (16, 31)]
+
+
+@pytest.mark.parametrize("n,variant", SLAB_VARIANTS)
+def test_semlap_slab_variants(cuda, n, variant):
+    """k-slab kernel tuning alternatives for the large orders."""
+    _sem_check(n, 53, fx.semlap_source(n, block=1), cuda, [(0, 53)],
+               variant=variant, seed=variant + n)
+
+
+@pytest.mark.parametrize("n", [3, 4, 5, 6, 7, 9, 10, 11])
+def test_semlap_slab_kernel_small_orders(cuda, n):
+    """Variant 9 forces the k-slab kernel for orders the chunk kernel
+    serves by default."""
+    _sem_check(n, 97, fx.semlap_source(n, block=1), cuda, [(0, 97)],
+               variant=9, seed=n)
+
+
 @pytest.mark.parametrize("n,nelt", [(5, 3), (7, 1), (9, 37), (15, 5),
-                                    (3, 101)])
+                                    (3, 101), (3, 6), (5, 11), (6, 7),
+                                    (2, 9)])
 def test_semlap_odd_order_tail(cuda, n, nelt):
     """Odd n and odd nelt: the last element's 16-byte-rounded u copy would
     run past the array, so the threads copy it themselves."""
