@@ -570,10 +570,6 @@ static int launch_cpa(double *w, const double *u, const double *d,
 
 // (n, variant) -> kernel.  variant 0 is the tuned default per order.
 #define LFB_SEM_TABLE(S, A)                                                 \
-  S(2, 0, 4, 3, false, false, false)                                        \
-  S(4, 0, 4, 3, false, false, false)                                        \
-  S(6, 0, 4, 3, false, false, false)                                        \
-  S(10, 0, 2, 1, true, false, false)                                        \
   S(8, 0, 4, 1, false, true, false)                                         \
   S(8, 1, 2, 3, false, false, false)                                        \
   S(8, 2, 4, 1, false, false, false)                                        \

@@ -43,19 +43,15 @@ struct GenCfg {
   static constexpr int STAGE = GPART + UPART;
 };
 
-// INPL: wr/ws of a point overwrite that point's g pair in the stage (the
-// owning thread has already read it), so no scratch is needed and a stage is
-// re-armed only after phase 2.
-template <int N, int E, int G, int S, bool INPL>
+template <int N, int E, int G, int S>
 struct GenSmem {
   using C = GenCfg<N, E>;
-  static constexpr int SCRD = INPL ? 0 : 2 * C::SCR;  // scratch per element
   static constexpr size_t bars = ((size_t)8 * G * S + 127) / 128 * 128;
   static constexpr size_t d_off = bars;
   static constexpr size_t scr_off =
       (d_off + 2 * (size_t)C::N2 * 8 + 127) / 128 * 128;
   static constexpr size_t stage_off =
-      (scr_off + (size_t)G * E * SCRD * 8 + 127) / 128 * 128;
+      (scr_off + (size_t)G * E * 2 * C::SCR * 8 + 127) / 128 * 128;
   static constexpr size_t total = stage_off + (size_t)G * S * C::STAGE * 8;
 };
 
@@ -70,14 +66,14 @@ __device__ __forceinline__ void ld_pair(const double *p, double &a,
   }
 }
 
-template <int N, int E, int G, int S, bool DREG, bool INPL, bool SUMSQ>
+template <int N, int E, int G, int S, bool DREG, bool SUMSQ>
 __global__ void __launch_bounds__(G *GenCfg<N, E>::T, 1)
     semlap_gen_kernel(double *__restrict__ w, const double *__restrict__ u,
                       const double *__restrict__ d,
                       const double *__restrict__ g, int64_t nelt,
                       double *__restrict__ partials) {
   using C = GenCfg<N, E>;
-  using L = GenSmem<N, E, G, S, INPL>;
+  using L = GenSmem<N, E, G, S>;
   constexpr int N2 = C::N2, NP = C::NP, T = C::T, R = C::R;
   static_assert(G <= 15, "named barrier ids 1..15");
 
@@ -144,7 +140,7 @@ __global__ void __launch_bounds__(G *GenCfg<N, E>::T, 1)
   }
   __syncthreads();
 
-  double *scr_r = scr + (size_t)(grp * E + el) * L::SCRD;
+  double *scr_r = scr + (size_t)(grp * E + el) * 2 * C::SCR;
   double *scr_s = scr_r + C::SCR;
   double acc = 0.0;
 
@@ -152,7 +148,7 @@ __global__ void __launch_bounds__(G *GenCfg<N, E>::T, 1)
     const int64_t c = chunk(m);
     const int st = grp * S + (int)(m % S);
     mbar_wait(&bars[st], (uint32_t)((m / S) & 1));
-    double *sg = stages + (size_t)st * C::STAGE;
+    const double *sg = stages + (size_t)st * C::STAGE;
     double *su0 = stages + (size_t)st * C::STAGE + C::GPART + u_lead(c);
     const int ne = chunk_elems(c);
     if (!u_bulk_ok(c)) {  // last chunk of an odd-n array: copy u by hand
@@ -161,7 +157,7 @@ __global__ void __launch_bounds__(G *GenCfg<N, E>::T, 1)
     }
     const bool active = lane_on && el < ne;
     const double *su = su0 + el * NP;
-    double *sge = sg + el * 6 * NP;
+    const double *sge = sg + el * 6 * NP;
 
     double wt[N];
     if (active) {
@@ -203,26 +199,20 @@ __global__ void __launch_bounds__(G *GenCfg<N, E>::T, 1)
           us = dadd(us, dmul(b0, col[N * l]));
           ut = dadd(ut, dmul(dk[l], ucol[l]));
         }
-        double *gp = sge + 6 * (i + N * j + N2 * k);
+        const double *gp = sge + 6 * (i + N * j + N2 * k);
         const double2 g01 = *reinterpret_cast<const double2 *>(gp);
         const double2 g23 = *reinterpret_cast<const double2 *>(gp + 2);
         const double2 g45 = *reinterpret_cast<const double2 *>(gp + 4);
-        const double wr =
+        scr_r[i + R * j + R * N * k] =
             dadd(dadd(dmul(g01.x, ur), dmul(g01.y, us)), dmul(g23.x, ut));
-        const double ws =
+        scr_s[i + R * j + R * N * k] =
             dadd(dadd(dmul(g01.y, ur), dmul(g23.y, us)), dmul(g45.x, ut));
-        if constexpr (INPL) {
-          *reinterpret_cast<double2 *>(gp) = make_double2(wr, ws);
-        } else {
-          scr_r[i + R * j + R * N * k] = wr;
-          scr_s[i + R * j + R * N * k] = ws;
-        }
         wt[k] = dadd(dadd(dmul(g23.x, ur), dmul(g45.x, us)), dmul(g45.y, ut));
       }
     }
     named_bar_sync(1 + grp, T);  // stage consumed, scratch complete
 
-    if (!INPL && lt == 0 && m + S < mine) {
+    if (lt == 0 && m + S < mine) {
       fence_proxy_async_smem();
       issue(st, chunk(m + S));
     }
@@ -236,38 +226,29 @@ __global__ void __launch_bounds__(G *GenCfg<N, E>::T, 1)
       double *we = w + (c * E + el) * NP + i + N * j;
 #pragma unroll
       for (int k = 0; k < N; ++k) {
-        // wr(., j, k) at rr[RS l], ws(i, ., k) at rs[SS l]
-        constexpr int RS = INPL ? 6 : 1;
-        constexpr int SS = INPL ? 6 * N : R;
-        const double *rr = INPL ? sge + 6 * (N * j + N2 * k)
-                                : scr_r + R * j + R * N * k;
-        const double *rs = INPL ? sge + 6 * (i + N2 * k) + 1
-                                : scr_s + i + R * N * k;
+        const double *rr = scr_r + R * j + R * N * k;  // wr(., j, k)
+        const double *rs = scr_s + i + R * N * k;      // ws(i, ., k)
         const double *dk = dn + N * k;                 // d(., k)
         double s = 0.0;
 #pragma unroll
         for (int l = 0; l + 1 < N; l += 2) {
           double r0, r1, k0, k1;
-          if constexpr (INPL) {
-            r0 = rr[RS * l], r1 = rr[RS * (l + 1)];
-          } else {
-            ld_pair<N>(rr + l, r0, r1);
-          }
+          ld_pair<N>(rr + l, r0, r1);
           ld_pair<N>(dk + l, k0, k1);
           const double a0 = DREG ? da[l] : dt[i + N * l];
           const double a1 = DREG ? da[l + 1] : dt[i + N * (l + 1)];
           const double b0 = DREG ? db[l] : dt[j + N * l];
           const double b1 = DREG ? db[l + 1] : dt[j + N * (l + 1)];
-          s = dadd(dadd(dadd(s, dmul(a0, r0)), dmul(b0, rs[SS * l])),
+          s = dadd(dadd(dadd(s, dmul(a0, r0)), dmul(b0, rs[R * l])),
                    dmul(k0, wt[l]));
-          s = dadd(dadd(dadd(s, dmul(a1, r1)), dmul(b1, rs[SS * (l + 1)])),
+          s = dadd(dadd(dadd(s, dmul(a1, r1)), dmul(b1, rs[R * (l + 1)])),
                    dmul(k1, wt[l + 1]));
         }
         if constexpr (N % 2 == 1) {
           constexpr int l = N - 1;
           const double a0 = DREG ? da[l] : dt[i + N * l];
           const double b0 = DREG ? db[l] : dt[j + N * l];
-          s = dadd(dadd(dadd(s, dmul(a0, rr[RS * l])), dmul(b0, rs[SS * l])),
+          s = dadd(dadd(dadd(s, dmul(a0, rr[l])), dmul(b0, rs[R * l])),
                    dmul(dk[l], wt[l]));
         }
         we[N2 * k] = s;
@@ -275,20 +256,16 @@ __global__ void __launch_bounds__(G *GenCfg<N, E>::T, 1)
       }
     }
     named_bar_sync(1 + grp, T);  // scratch reads done before the next chunk
-    if (INPL && lt == 0 && m + S < mine) {
-      fence_proxy_async_smem();
-      issue(st, chunk(m + S));
-    }
   }
 
   if constexpr (SUMSQ) block_sumsq_partial(acc, partials);
 }
 
-template <int N, int E, int G, int S, bool DREG, bool INPL>
+template <int N, int E, int G, int S, bool DREG>
 static int launch_gen(double *w, const double *u, const double *d,
                       const double *g, int64_t nelt, const lfb_launch *geom,
                       cudaStream_t s, int64_t *grid_out) {
-  using L = GenSmem<N, E, G, S, INPL>;
+  using L = GenSmem<N, E, G, S>;
   static_assert(L::total <= 227 * 1024, "smem");
   constexpr int block = G * GenCfg<N, E>::T;
   int sms = sm_count(geom);
@@ -306,8 +283,8 @@ static int launch_gen(double *w, const double *u, const double *d,
   const bool sumsq = geom && geom->sumsq;
   if (sumsq && (!geom->workspace || geom->workspace_len < grid))
     return fail(LFB_ERR_ARG, "semlap: sumsq workspace too small");
-  auto k = sumsq ? semlap_gen_kernel<N, E, G, S, DREG, INPL, true>
-                 : semlap_gen_kernel<N, E, G, S, DREG, INPL, false>;
+  auto k = sumsq ? semlap_gen_kernel<N, E, G, S, DREG, true>
+                 : semlap_gen_kernel<N, E, G, S, DREG, false>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)L::total);
   k<<<grid, block, L::total, s>>>(w, u, d, g, nelt,
@@ -317,49 +294,48 @@ static int launch_gen(double *w, const double *u, const double *d,
                : LFB_OK;
 }
 
-// (n, variant) -> (E, G, S, DREG, INPL); variant 0 = default for that n
-// (round-1 B200 sweep, profiles/r01/sem_sweep.jsonl)
-#define LFB_GEN_TABLE(X)               \
-  X(2, 0, 8, 8, 1, true, false)        \
-  X(3, 0, 7, 8, 1, true, false)        \
-  X(4, 0, 2, 14, 1, true, false)       \
-  X(4, 20, 2, 8, 3, true, false)       \
-  X(4, 21, 4, 6, 2, true, false)       \
-  X(4, 23, 2, 14, 1, true, true)       \
-  X(5, 0, 5, 3, 1, true, false)        \
-  X(5, 20, 5, 4, 1, true, false)       \
-  X(5, 21, 5, 4, 1, true, true)        \
-  X(5, 22, 5, 2, 2, true, false)       \
-  X(6, 0, 3, 4, 1, true, false)        \
-  X(6, 20, 2, 6, 1, true, false)       \
-  X(6, 21, 1, 12, 1, true, false)      \
-  X(6, 22, 3, 6, 1, true, true)        \
-  X(7, 0, 2, 3, 1, true, false)        \
-  X(7, 20, 1, 8, 1, true, false)       \
-  X(7, 21, 2, 4, 1, true, false)       \
-  X(7, 22, 1, 11, 1, true, true)       \
-  X(7, 23, 2, 5, 1, true, true)        \
-  X(8, 20, 1, 3, 2, true, false)       \
-  X(8, 21, 1, 4, 1, true, false)       \
-  X(8, 22, 1, 6, 1, true, true)        \
-  X(9, 0, 1, 4, 1, false, false)       \
-  X(9, 20, 1, 5, 1, false, true)       \
-  X(9, 21, 1, 5, 1, true, true)        \
-  X(10, 0, 1, 3, 1, false, false)      \
-  X(10, 20, 1, 4, 1, false, true)      \
-  X(10, 21, 1, 4, 1, true, true)       \
-  X(11, 0, 1, 2, 1, true, false)       \
-  X(11, 20, 1, 3, 1, false, true)      \
-  X(12, 20, 1, 2, 1, false, true)
+// (n, variant) -> (E, G, S, DREG); variant 0 = default for that n, from the
+// round-1 B200 sweep (profiles/r01/sem_sweep.jsonl).  One stage per group
+// (re-armed after phase 1, so the load overlaps phase 2 and the other
+// groups) with as many groups as smem allows beat deeper rings everywhere.
+#define LFB_GEN_TABLE(X)        \
+  X(2, 0, 8, 8, 1, true)        \
+  X(3, 0, 7, 8, 1, true)        \
+  X(4, 0, 2, 14, 1, true)       \
+  X(4, 20, 2, 8, 3, true)       \
+  X(4, 21, 4, 6, 2, true)       \
+  X(5, 0, 5, 4, 1, true)        \
+  X(5, 20, 5, 3, 1, true)       \
+  X(5, 21, 1, 14, 2, true)      \
+  X(5, 22, 5, 2, 2, true)       \
+  X(6, 0, 3, 4, 1, true)        \
+  X(6, 20, 2, 6, 1, true)       \
+  X(6, 21, 1, 8, 2, true)       \
+  X(6, 22, 2, 4, 2, true)       \
+  X(7, 0, 2, 4, 1, true)        \
+  X(7, 20, 2, 3, 1, true)       \
+  X(7, 21, 1, 8, 1, true)       \
+  X(7, 22, 1, 5, 2, true)       \
+  X(8, 20, 1, 3, 2, true)       \
+  X(8, 21, 1, 4, 1, true)       \
+  X(8, 22, 1, 4, 1, false)      \
+  X(9, 0, 1, 4, 1, false)       \
+  X(9, 20, 1, 2, 2, true)       \
+  X(9, 21, 1, 3, 1, true)       \
+  X(10, 0, 1, 3, 1, false)      \
+  X(10, 20, 1, 2, 1, true)      \
+  X(10, 21, 1, 3, 1, true)      \
+  X(11, 0, 1, 2, 1, true)       \
+  X(11, 20, 1, 2, 1, false)
 
 int sem_gen_dispatch(int n, int variant, double *w, const double *u,
                      const double *d, const double *g, int64_t nelt,
                      const lfb_launch *geom, cudaStream_t s,
                      int64_t *grid_out) {
-#define X(NN, VV, EE, GG, SS, DR, IP)                                      \
+#define X(NN, VV, EE, GG, SS, DR)                                          \
   if (n == NN && variant == VV)                                            \
-    return launch_gen<NN, EE, GG, SS, DR, IP>(w, u, d, g, nelt, geom, s,   \
-                                              grid_out);
+    return launch_gen<NN, EE, GG, SS, DR>(w, u, d, g, nelt, geom, s,       \
+                                          grid_out);
   LFB_GEN_TABLE(X)
 #undef X
   return -1;  // no generic-kernel entry for (n, variant)
