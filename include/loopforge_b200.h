@@ -124,6 +124,27 @@ int lfb_sgemm_f32(float alpha, const float *a, const float *b, float *c,
  * possible else the bit-exact CUDA-core kernel, 1 bit-exact, 2 tensor only */
 int64_t lfb_sgemm_workspace(int l, int m, int n);
 
+/* Generic path: CUDA C++ generated from a kernel's
+ * schedule by paper_1503_07659_b200/cudagen.py -- g.N -> blockIdx, l.N ->
+ * threadIdx, workgroup temporaries -> __shared__ with real barriers -- the
+ * executable counterpart of the OpenCL text the reference only prints
+ * (codegen.py:580-612, 707-710).  Compiled for sm_100a by NVRTC (dlopen'ed),
+ * loaded and launched through the driver API.
+ *
+ * lfb_rtc_compile: cubin == NULL queries the size into *cubin_len; otherwise
+ * writes at most *cubin_len bytes.  Compiler diagnostics -> lfb_last_error. */
+typedef struct lfb_module_st *lfb_module;
+int lfb_rtc_compile(const char *src, const char *prog_name,
+                    const char *const *opts, int nopts, void *cubin,
+                    int64_t *cubin_len);
+int lfb_module_load(const void *cubin, int64_t len, const char *kernel_name,
+                    lfb_module *out);
+/* grid/block: 3 extents each (the g.N / l.N extents); args: cuLaunchKernel
+ * argument pointers in the generated kernel's parameter order. */
+int lfb_module_launch(lfb_module m, const int64_t *grid, const int32_t *block,
+                      int32_t smem, void **args, lfb_stream stream);
+int lfb_module_unload(lfb_module m);
+
 /* Microbenchmark used by bench.py to state the FP64 issue ceiling the SEM
  * kernel runs against: iters x 8 independent DMUL+DADD chains per thread. */
 int lfb_probe_fp64(double *out, int iters, int blocks, int threads,

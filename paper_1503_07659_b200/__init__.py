@@ -3,7 +3,9 @@
 The reference (arXiv 1503.07659's Loo.py, re-created as ``loopforge``) keeps
 its Fortran-subset front end and transform library; this package replaces
 the execution step -- ``loopforge.interp.interpret`` -- with hand-written
-sm_100a kernels behind a C ABI (include/loopforge_b200.h)::
+sm_100a kernels behind a C ABI (include/loopforge_b200.h), and -- for kernels
+outside that set -- with CUDA generated from the kernel's schedule
+(cudagen.py, compiled by NVRTC for sm_100a)::
 
     from loopforge.fortran import translate_file_text
     import paper_1503_07659_b200 as lfb
@@ -16,13 +18,16 @@ sm_100a kernels behind a C ABI (include/loopforge_b200.h)::
 See DESIGN.md for the kernels and INTEGRATION.md for the ABI bindings.
 """
 
-from .executor import (DeviceArray, DeviceEnv, Launcher, env_from_buffers,
-                       flat_outputs, get_device_output, get_output,
-                       interpret, make_device_env, plan_for)
+from .cudagen import emit_cuda
+from .executor import (ENGINES, DeviceArray, DeviceEnv, Launcher,
+                       env_from_buffers, flat_outputs, get_device_output,
+                       get_output, interpret, make_device_env, make_launcher,
+                       plan_for)
 from .launch import Geometry, launch_geometry
 from .recognize import WORKLOADS, canonicalize, recognize
 
 __all__ = [
+    "ENGINES", "emit_cuda", "make_launcher",
     "DeviceArray", "DeviceEnv", "Launcher", "env_from_buffers",
     "flat_outputs", "get_device_output", "get_output", "interpret",
     "make_device_env", "plan_for", "Geometry", "launch_geometry",

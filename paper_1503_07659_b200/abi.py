@@ -57,6 +57,12 @@ SIGNATURES = {
     "lfb_sgemm_workspace": [I32, I32, I32],
     "lfb_probe_fp64": [P, I32, I32, I32, P],
     "lfb_probe_stream": [P, P, P, C.c_int64, P],
+    "lfb_rtc_compile": [C.c_char_p, C.c_char_p, C.POINTER(C.c_char_p), I32,
+                        P, C.POINTER(C.c_int64)],
+    "lfb_module_load": [P, C.c_int64, C.c_char_p, C.POINTER(P)],
+    "lfb_module_launch": [P, C.POINTER(C.c_int64), C.POINTER(C.c_int32),
+                          C.c_int32, C.POINTER(P), P],
+    "lfb_module_unload": [P],
 }
 _RESTYPES = {"lfb_last_error": C.c_char_p, "lfb_semlap_workspace": C.c_int64,
              "lfb_sgemm_workspace": C.c_int64}

@@ -72,7 +72,7 @@ def build(force=False, verbose=False):
             os.path.getmtime(LIB) >= max(os.path.getmtime(o) for o in objs):
         return LIB
     cmd = [nvcc()] + ARCH + ["-shared", "-o", LIB] + objs + \
-        ["-cudart", "static"]
+        ["-cudart", "static", "-ldl"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"link failed:\n{res.stderr[-4000:]}")

@@ -270,7 +270,38 @@ class Launcher:
         abi.check(rc, f"{fam}_{dt}")
 
 
-def interpret(kernel, env, inplace=False, variant=0, stream=None):
+ENGINES = ("auto", "kernels", "generic")
+
+
+def make_launcher(kernel, env, variant=0, engine="auto"):
+    """The launcher for *kernel*.
+
+    ``engine="kernels"``: the hand-written sm_100a kernel of the recognised
+    workload, else ``CodegenError``.  ``"generic"``: CUDA generated from the
+    kernel's schedule (cudagen.py).  ``"auto"`` (default): the hand-written
+    kernel when the recognizer matches, otherwise the generated one.  Both
+    run on the device; there is no CPU path.
+    """
+    if engine not in ENGINES:
+        raise CodegenError(f"unknown engine {engine!r}; one of {ENGINES}")
+    if engine == "generic":
+        from .generic import GenericLauncher
+        return GenericLauncher(kernel, env)
+    try:
+        return Launcher(kernel, env, variant=variant)
+    except CodegenError as exc:
+        if engine == "kernels":
+            raise
+        from .generic import GenericLauncher
+        try:
+            return GenericLauncher(kernel, env)
+        except CodegenError as exc2:
+            raise CodegenError(f"{exc}; generic CUDA emitter: {exc2} "
+                               "(no CPU fallback)") from exc2
+
+
+def interpret(kernel, env, inplace=False, variant=0, stream=None,
+              engine="auto"):
     """Run *kernel* on the B200 (drop-in for interp.py:323).
 
     Returns a new :class:`DeviceEnv` whose output arrays hold the results;
@@ -283,7 +314,8 @@ def interpret(kernel, env, inplace=False, variant=0, stream=None):
         for a in kernel.args:
             if a.kind == "global-array" and a.is_output:
                 out.arrays[a.name] = env.arrays[a.name].copy()
-    Launcher(kernel, out, variant=variant).launch(stream=stream)
+    make_launcher(kernel, out, variant=variant, engine=engine).launch(
+        stream=stream)
     return out
 
 

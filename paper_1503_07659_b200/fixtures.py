@@ -198,3 +198,148 @@ def translate(source, name="<fixture>"):
     from ._loopforge import fortran
     raw, transformed, _unit = fortran.translate_file_text(source, name)
     return raw, transformed
+
+
+# {{{ kernels for the generic path (cudagen.py)
+#
+# Fortran-ingested kernels outside the hand-written set, each exercising one
+# piece of the reference semantics the generated CUDA must reproduce:
+# predicates from if/else (lowering: fortran.py:484-498), transcendental
+# calls, workgroup precompute tiles with barriers (the paper's DGEMM in
+# real*8, test_fortran.py:72-103), numpy type promotion of mixed int/real*4
+# arithmetic (interp.py:169-187), 2-D g/l tags with a residual guard, int32
+# arithmetic, a stencil, and native-language reductions (interp.py:213-248).
+
+_SPLIT = ('! {k} = lp.split_iname({k}, "{i}", {b}, outer_tag="g.{a}", '
+          'inner_tag="l.{a}")\n')
+
+GENERIC_FORTRAN = {
+    # the reference's COND_F (test_fortran.py:29-48) with a launch script
+    "cond": ("""subroutine cond(out, inp, n)
+  implicit none
+  real*8 out(n), inp(n), a, b
+  integer n, i, j
+
+  do i = 1, n
+    a = inp(i)
+    if (a.ge.0.25) then
+        b = 2*a
+        do j = 1,3
+            b = 3 * b
+        end do
+        out(i) = 5*b
+    else
+        out(i) = 4*a
+    endif
+  end do
+end
+""", [_SPLIT.format(k="cond", i="i", b=64, a=0)]),
+    # the reference's TAGGED_F body (rotnorm: sin, cos, sqrt, division)
+    "rotnorm": ("""subroutine rotnorm(out1, out2, inp1, inp2, alpha, n)
+  implicit none
+  real*8 out1(n), out2(n), inp1(n), inp2(n), alpha, a, b, r
+  integer n, i
+
+  do i = 1, n
+    a = cos(alpha)*inp1(i) + sin(alpha)*inp2(i)
+    b = -sin(alpha)*inp1(i) + cos(alpha)*inp2(i)
+    r = sqrt(a**2 + b**2)
+    a = a/r
+    b = b/r
+    out1(i) = a
+    out2(i) = b
+  end do
+end
+""", [_SPLIT.format(k="rotnorm", i="i", b=128, a=0)]),
+    # int/real*4 mixing: numpy computes int32 op float32 in float64
+    "mixed": ("""subroutine mixed(y, z, x, n)
+  implicit none
+  real*4 y(n), z(n), x(n)
+  integer n, i
+
+  do i = 1, n
+    y(i) = x(i)*i + 0.5
+    z(i) = x(i)/3 - 2*x(i)**2
+  end do
+end
+""", [_SPLIT.format(k="mixed", i="i", b=32, a=0)]),
+    "stencil": ("""subroutine stencil(r, u, n)
+  implicit none
+  real*4 r(n), u(n+1)
+  integer n, i
+
+  do i = 1, n
+    r(i) = u(i+1) - u(i)
+  end do
+end
+""", [_SPLIT.format(k="stencil", i="i", b=96, a=0)]),
+    "transpose": ("""subroutine transpose(b, a, n, m)
+  implicit none
+  real*8 b(m,n), a(n,m)
+  integer n, m, i, j
+
+  do j = 1, m
+    do i = 1, n
+      b(j,i) = 2*a(i,j) - 1
+    end do
+  end do
+end
+""", [_SPLIT.format(k="transpose", i="i", b=16, a=0),
+      _SPLIT.format(k="transpose", i="j", b=8, a=1)]),
+    "intops": ("""subroutine intops(k, j, n)
+  implicit none
+  integer n, i, k(n), j(n)
+
+  do i = 1, n
+    k(i) = j(i)*3 + i*i - 7
+  end do
+end
+""", [_SPLIT.format(k="intops", i="i", b=64, a=0)]),
+    # matvec with the accumulation order of a user's own variant (y
+    # accumulated in place): outside the recognizer's templates
+    "matvec_acc": ("""subroutine mvacc(y, a, x, n)
+  implicit none
+  real*8 y(n), a(n,n), x(n)
+  integer n, i, j
+
+  do i = 1, n
+    do j = 1, n
+      y(i) = y(i) + x(j)*a(i,j)
+    end do
+  end do
+end
+""", [_SPLIT.format(k="mvacc", i="i", b=32, a=0),
+      '! mvacc = lp.split_iname(mvacc, "j", 16)\n',
+      '! mvacc = lp.extract_subst(mvacc, "x_acc", "x[jj]", '
+      'parameters="jj")\n',
+      '! mvacc = lp.precompute(mvacc, "x_acc", "j_inner")\n']),
+}
+
+# native-language kernels (kernel.py:323 make_kernel): reductions
+GENERIC_NATIVE = {
+    "rowsum": (["{[i,j]: 0<=i<n and 0<=j<m}"],
+               "out[i] = sum(j, a[i,j]*b[j])\n"
+               "lo[i] = min(j, a[i,j])\nhi[i] = max(j, a[i,j])",
+               [("i", 32, "g.0", "l.0")]),
+}
+
+
+def generic_source(name):
+    """Fortran text (+ script) of a generic-path fixture."""
+    body, lines = GENERIC_FORTRAN[name]
+    return body + _block(lines)
+
+
+def generic_native(name):
+    """(raw, transformed) native-language kernels of a generic fixture."""
+    from ._loopforge import kernel as lfk, transforms
+    domains, body, splits = GENERIC_NATIVE[name]
+    raw = lfk.make_kernel(domains, body, name=name,
+                          dtype_default=lfk.F64)
+    knl = raw
+    for iname, factor, outer, inner in splits:
+        knl = transforms.split_iname(knl, iname, factor, outer_tag=outer,
+                                     inner_tag=inner)
+    return raw, knl
+
+# }}}

@@ -1,0 +1,116 @@
+"""Generic execution path: schedule -> CUDA (cudagen) -> NVRTC -> launch.
+
+For kernels outside the hand-written set (recognize.py).  Compiles once per
+distinct generated source (in-process cache keyed by its hash), loads the
+cubin into the current CUDA context and launches it with the reference's
+logical geometry: grid = the g.N extents, CTA = the l.N extents
+(launch.py / codegen.py:580-612).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+
+from . import abi
+from .cudagen import NVRTC_OPTIONS, emit_cuda
+from .launch import launch_geometry
+
+_CUBINS = {}    # program key -> cubin bytes
+_MODULES = {}   # (program key, device index) -> lfb_module handle
+_PROGRAMS = {}  # id(kernel) -> (kernel, Program)
+
+
+def program_for(kernel):
+    hit = _PROGRAMS.get(id(kernel))
+    if hit is not None and hit[0] is kernel:
+        return hit[1]
+    prog = emit_cuda(kernel)
+    if len(_PROGRAMS) > 256:
+        _PROGRAMS.clear()
+    _PROGRAMS[id(kernel)] = (kernel, prog)
+    return prog
+
+
+def compile_program(prog):
+    """NVRTC -> sm_100a cubin (no device needed)."""
+    cub = _CUBINS.get(prog.key)
+    if cub is not None:
+        return cub
+    lib = abi.load()
+    opts = (C.c_char_p * len(NVRTC_OPTIONS))(
+        *[o.encode() for o in NVRTC_OPTIONS])
+    n = C.c_int64(0)
+    abi.check(lib.lfb_rtc_compile(prog.source.encode(),
+                                  f"{prog.entry}.cu".encode(), opts,
+                                  len(NVRTC_OPTIONS), None, C.byref(n)),
+              f"NVRTC {prog.entry}")
+    buf = C.create_string_buffer(n.value)
+    abi.check(lib.lfb_rtc_compile(prog.source.encode(),
+                                  f"{prog.entry}.cu".encode(), opts,
+                                  len(NVRTC_OPTIONS), buf, C.byref(n)),
+              f"NVRTC {prog.entry}")
+    cub = buf.raw[:n.value]
+    _CUBINS[prog.key] = cub
+    return cub
+
+
+def _module(prog, device_index):
+    key = (prog.key, device_index)
+    mod = _MODULES.get(key)
+    if mod is None:
+        cub = compile_program(prog)
+        h = C.c_void_p()
+        abi.check(abi.load().lfb_module_load(cub, len(cub),
+                                             prog.entry.encode(),
+                                             C.byref(h)),
+                  f"load {prog.entry}")
+        mod = h
+        _MODULES[key] = mod
+    return mod
+
+
+_CTY = {"f64": C.c_double, "f32": C.c_float, "i32": C.c_int32}
+
+
+class GenericLauncher:
+    """Prepared launch of the generated kernel (same interface as
+    executor.Launcher)."""
+
+    def __init__(self, kernel, env):
+        self.kernel = kernel
+        self.env = env
+        self.program = program_for(kernel)
+        self.geometry = launch_geometry(kernel, env.params)
+
+    def launch(self, env=None, stream=None):
+        env = env or self.env
+        prog = self.program
+        dev = env.device if env.device is not None else torch.device(
+            "cuda", torch.cuda.current_device())
+        with torch.cuda.device(dev):
+            mod = _module(prog, dev.index)
+            if stream is None:
+                stream = torch.cuda.current_stream(dev).cuda_stream
+        vals = []
+        args = {a.name: a for a in self.kernel.args}
+        for name in prog.arg_order:
+            a = args.get(name)
+            if a is None:                      # a parameter (int64)
+                vals.append(C.c_int64(int(env.params[name])))
+            elif a.kind == "global-array":
+                vals.append(C.c_void_p(env.arrays[name].data.data_ptr()))
+            else:
+                vals.append(_CTY[a.dtype](env.scalars[name]))
+        argv = (C.c_void_p * len(vals))(
+            *[C.cast(C.pointer(v), C.c_void_p) for v in vals])
+        geo = self.geometry
+        grid = (C.c_int64 * 3)(*geo.group_extent)
+        block = (C.c_int32 * 3)(*prog.block)
+        abi.check(abi.load().lfb_module_launch(mod, grid, block, 0, argv,
+                                               stream),
+                  f"launch {prog.entry}")
+
+
+__all__ = ["GenericLauncher", "program_for", "compile_program"]

@@ -53,6 +53,8 @@ class Golden:
 
     def kernels(self):
         from paper_1503_07659_b200 import fixtures
+        if self.meta["generator"] == "generic_native":
+            return fixtures.generic_native(**self.meta["kwargs"])
         return fixtures.translate(self.source(), f"{self.name}.f")
 
     def outputs(self):

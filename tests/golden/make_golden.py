@@ -61,15 +61,42 @@ CASES = {
                          {"m": 16, "n": 8, "l": 32}, {"alpha": 1.5}, 7),
     "sgemm_m20_n12_l40": ("gemm_source", {"dtype": "f32"},
                           {"m": 20, "n": 12, "l": 40}, {"alpha": -0.5}, 8),
+    # generic path (cudagen.py): kernels outside the hand-written set
+    "gen_cond_n300": ("generic_source", {"name": "cond"}, {"n": 300}, {}, 11),
+    "gen_rotnorm_n300": ("generic_source", {"name": "rotnorm"}, {"n": 300},
+                         {"alpha": 0.3}, 12),
+    "gen_mixed_n333": ("generic_source", {"name": "mixed"}, {"n": 333}, {},
+                       13),
+    "gen_stencil_n250": ("generic_source", {"name": "stencil"}, {"n": 250},
+                         {}, 14),
+    "gen_transpose_n37_m21": ("generic_source", {"name": "transpose"},
+                              {"n": 37, "m": 21}, {}, 15),
+    "gen_intops_n200": ("generic_source", {"name": "intops"}, {"n": 200},
+                        {}, 16),
+    "gen_mvacc_n64": ("generic_source", {"name": "matvec_acc"}, {"n": 64},
+                      {}, 17),
+    "gen_dgemm_m20_n12_l40": ("gemm_source", {"dtype": "f64"},
+                              {"m": 20, "n": 12, "l": 40}, {"alpha": 0.75},
+                              18),
+    "gen_rowsum_n40_m17": ("generic_native", {"name": "rowsum"},
+                           {"n": 40, "m": 17}, {}, 19),
 }
+
+# in/out arrays: outputs that are also read (make_env never randomises
+# outputs, interp.py:115, so they get values from a second stream)
+INOUT = {"gemm_source": "c", "axpy_source": "y",
+         ("generic_source", "matvec_acc"): "y"}
 
 
 def build_case(name, spec):
     gen, kwargs, params, explicit, seed = spec
-    src = getattr(fx, gen)(**kwargs)
-    _raw, knl = fx.translate(src, f"{name}.f")
+    if gen == "generic_native":
+        _raw, knl = fx.generic_native(**kwargs)
+    else:
+        src = getattr(fx, gen)(**kwargs)
+        _raw, knl = fx.translate(src, f"{name}.f")
     inputs = dict(explicit)
-    inout = {"gemm_source": "c", "axpy_source": "y"}.get(gen)
+    inout = INOUT.get(gen) or INOUT.get((gen, kwargs.get("name")))
     if inout:
         # in/out arrays are outputs, which make_env never randomises
         # (interp.py:115): give them values from a second stream

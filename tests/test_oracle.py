@@ -40,7 +40,8 @@ def _run_oracle(g):
     raise AssertionError(fam)
 
 
-@pytest.mark.parametrize("name", golden_names())
+@pytest.mark.parametrize("name", [n for n in golden_names()
+                                  if not n.startswith("gen_")])
 def test_oracle_matches_reference_interpreter(name):
     g = Golden(name)
     got = _run_oracle(g)
