@@ -294,9 +294,17 @@ def test_unrecognised_kernel_is_codegen_error(cuda):
     src = fx.axpy_source("f64").replace("y(i) + alpha*x(i)",
                                         "y(i) + x(i)*alpha")
     _r, knl = fx.translate(src)
-    env = lfb.make_device_env(knl, {"n": 256}, device=cuda)
+    env = lfb.make_device_env(knl, {"n": 256}, {"alpha": 1.7}, seed=1,
+                              device=cuda)
     with pytest.raises(CodegenError, match="no CPU fallback"):
-        lfb.interpret(knl, env)
+        lfb.interpret(knl, env, engine="kernels")
+    # the default engine runs it as generated CUDA instead (test_generic.py)
+    out = lfb.interpret(knl, env)
+    y = env.arrays["y"].data.cpu().numpy()
+    x = env.arrays["x"].data.cpu().numpy()
+    alpha = env.scalars["alpha"]
+    assert out.arrays["y"].data.cpu().numpy().tobytes() == \
+        (y + x * alpha).tobytes()
 
 
 def test_wrong_shape_input_is_interp_error(cuda):
