@@ -116,19 +116,19 @@ __host__ __device__ constexpr uint32_t tf32_idesc(int M, int N) {
   asm volatile(                                                              \
       "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "                        \
       "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"            \
-      ::"r"(taddr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]),   \
-      "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]), "r"(r[10]),     \
-      "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])             \
+      ::"r"(taddr), "r"((r)[0]), "r"((r)[1]), "r"((r)[2]), "r"((r)[3]), "r"((r)[4]),   \
+      "r"((r)[5]), "r"((r)[6]), "r"((r)[7]), "r"((r)[8]), "r"((r)[9]), "r"((r)[10]),     \
+      "r"((r)[11]), "r"((r)[12]), "r"((r)[13]), "r"((r)[14]), "r"((r)[15])             \
       : "memory")
 
 #define LFB_TMEM_LD16(taddr, r)                                              \
   asm volatile(                                                              \
       "tcgen05.ld.sync.aligned.32x32b.x16.b32 "                              \
       "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"      \
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]),          \
-        "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]),          \
-        "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),     \
-        "=r"(r[15])                                                          \
+      : "=r"((r)[0]), "=r"((r)[1]), "=r"((r)[2]), "=r"((r)[3]), "=r"((r)[4]),          \
+        "=r"((r)[5]), "=r"((r)[6]), "=r"((r)[7]), "=r"((r)[8]), "=r"((r)[9]),          \
+        "=r"((r)[10]), "=r"((r)[11]), "=r"((r)[12]), "=r"((r)[13]), "=r"((r)[14]),     \
+        "=r"((r)[15])                                                          \
       : "r"(taddr))
 
 // }}}
@@ -289,6 +289,211 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   }
 }
 
+// {{{ persistent kernel: overlapped epilogue, 8-warp chunk folds
+//
+// sgemm_tc_kernel above runs one tile per CTA and ends every tile with a
+// serial C read-modify-write that leaves the tensor pipe idle (ncu: tensor
+// pipe 49 % active, a fifth of all stall samples on the epilogue's C loads,
+// profiles/r01_sgemm.md).  Here
+//  * CTAs are persistent (one per SM) over a grouped tile order: while the
+//    epilogue warps fold the last chunk of tile t and update C, the MMA warp
+//    already accumulates chunk 0 of tile t + 1 (A is free as soon as the
+//    last fold has read it; T is reused only by the next tile's first fold,
+//    one chunk later);
+//  * 8 epilogue warps (warp w: TMEM lane quarter w % 4, column half
+//    (w - 2) / 4) fold each chunk twice as fast as 4, shortening the MMA
+//    warp's wait at chunk boundaries;
+//  * the C update keeps 32 loads per thread in flight.
+// Numerics are unchanged: T = A_0, T = T + A_1, ... (round-to-nearest FADD),
+// c = c + alpha*T.
+constexpr int TC2_THREADS = 320;  // producer, MMA, 8 epilogue warps
+constexpr int TC2_GROUP_M = 8;    // M tiles per raster group
+
+__device__ __forceinline__ void tc2_tile(int t, int mt_count, int nt_count,
+                                         int *mt, int *nt) {
+  const int per_group = TC2_GROUP_M * nt_count;
+  const int grp = t / per_group;
+  const int r = t % per_group;
+  const int m0 = grp * TC2_GROUP_M;
+  const int gm = min(TC2_GROUP_M, mt_count - m0);
+  *mt = m0 + r % gm;
+  *nt = r / gm;
+}
+
+__global__ void __launch_bounds__(TC2_THREADS, 1)
+    sgemm_tc2_kernel(const __grid_constant__ CUtensorMap map_ahi,
+                     const __grid_constant__ CUtensorMap map_alo,
+                     const __grid_constant__ CUtensorMap map_bhi,
+                     const __grid_constant__ CUtensorMap map_blo, float alpha,
+                     float *__restrict__ c, int l, int m, int n) {
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char *smem = reinterpret_cast<unsigned char *>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + TcSmem::bars_off);
+  uint64_t *empty = full + TC_STAGES;
+  uint64_t *acc_full = empty + TC_STAGES;  // MMA -> epilogue: chunk in A
+  uint64_t *acc_empty = acc_full + 1;      // epilogue -> MMA: A folded
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(acc_empty + 1);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int nk = l / TC_BK;
+  const int nchunks = (nk + TC_CHUNK - 1) / TC_CHUNK;
+  const int mt_count = m / TC_BM, nt_count = n / TC_BN;
+  const int ntiles = mt_count * nt_count;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < TC_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(acc_full, 1);
+    mbar_init(acc_empty, 8);  // one arrive per epilogue warp
+    fence_mbar_init();
+  }
+  if (warp == 1) {
+    asm volatile(
+        "tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+        ::"r"(smem_u32(tmem_slot)), "r"(TC_TMEM_COLS)
+        : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;"
+                 ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;  // A: columns 0..255, T: 256..511
+
+  auto stage_ptr = [&](int s) { return smem + s * TcSmem::stage_bytes; };
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int it = 0;  // k-slab counter over all tiles of this CTA
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        int mt, nt;
+        tc2_tile(t, mt_count, nt_count, &mt, &nt);
+        const int i0 = mt * TC_BM, j0 = nt * TC_BN;
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int s = it % TC_STAGES;
+          mbar_wait(&empty[s], ((it / TC_STAGES) & 1) ^ 1);
+          unsigned char *st = stage_ptr(s);
+          mbar_arrive_expect_tx(&full[s], (uint32_t)TcSmem::stage_bytes);
+          const int k0 = kb * TC_BK;
+          tma_load_2d(st, &map_ahi, k0, i0, &full[s]);
+          tma_load_2d(st + TcSmem::a_bytes, &map_alo, k0, i0, &full[s]);
+          tma_load_2d(st + 2 * TcSmem::a_bytes, &map_bhi, k0, j0, &full[s]);
+          tma_load_2d(st + 2 * TcSmem::a_bytes + TcSmem::b_bytes, &map_blo,
+                      k0, j0, &full[s]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc = tf32_idesc(TC_BM, TC_BN);
+    int it = 0, g = 0;  // k-slab and chunk counters over all tiles
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      for (int kb = 0; kb < nk; ++kb, ++it) {
+        const int s = it % TC_STAGES;
+        const bool first_in_chunk = (kb % TC_CHUNK) == 0;
+        const bool last_in_chunk =
+            kb % TC_CHUNK == TC_CHUNK - 1 || kb == nk - 1;
+        if (first_in_chunk && g > 0)  // chunk g - 1 folded out of A
+          mbar_wait(acc_empty, (g - 1) & 1);
+        mbar_wait(&full[s], (it / TC_STAGES) & 1);
+        tc_fence_after();
+        if (lane == 0) {
+          unsigned char *st = stage_ptr(s);
+          const uint64_t ahi = sw128_kmajor_desc(st);
+          const uint64_t alo = sw128_kmajor_desc(st + TcSmem::a_bytes);
+          const uint64_t bhi = sw128_kmajor_desc(st + 2 * TcSmem::a_bytes);
+          const uint64_t blo =
+              sw128_kmajor_desc(st + 2 * TcSmem::a_bytes + TcSmem::b_bytes);
+#pragma unroll
+          for (int k = 0; k < TC_BK / 8; ++k) {
+            const uint64_t dk = (uint64_t)((k * 32) >> 4);
+            tc_mma_tf32(tmem, alo + dk, bhi + dk, idesc,
+                        !(first_in_chunk && k == 0));
+            tc_mma_tf32(tmem, ahi + dk, blo + dk, idesc, 1);
+            tc_mma_tf32(tmem, ahi + dk, bhi + dk, idesc, 1);
+          }
+          tc_commit(&empty[s]);
+          if (last_in_chunk) tc_commit(acc_full);
+        }
+        __syncwarp();
+        if (last_in_chunk) ++g;
+      }
+    }
+  } else {
+    const int q = warp % 4;
+    const int h = (warp - 2) / 4;  // column half
+    const uint32_t lanes = (uint32_t)(q * 32) << 16;
+    const uint32_t ta = tmem + lanes + (uint32_t)(h * 128);
+    const uint32_t tt = ta + TC_BN;
+    int g = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      int mt, nt;
+      tc2_tile(t, mt_count, nt_count, &mt, &nt);
+      for (int ch = 0; ch < nchunks; ++ch, ++g) {
+        mbar_wait(acc_full, g & 1);
+        tc_fence_after();
+        // T = A (first chunk) or T = T + A, round to nearest
+#pragma unroll 1
+        for (int cb = 0; cb < 128; cb += 32) {
+          uint32_t ra[32], rt[32];
+          LFB_TMEM_LD16(ta + cb, ra);
+          LFB_TMEM_LD16(ta + cb + 16, ra + 16);
+          if (ch > 0) {
+            LFB_TMEM_LD16(tt + cb, rt);
+            LFB_TMEM_LD16(tt + cb + 16, rt + 16);
+          }
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+          for (int x = 0; x < 32; ++x)
+            rt[x] = ch > 0 ? __float_as_uint(fadd(__uint_as_float(rt[x]),
+                                                  __uint_as_float(ra[x])))
+                           : ra[x];
+          LFB_TMEM_ST16(tt + cb, rt);
+          LFB_TMEM_ST16(tt + cb + 16, rt + 16);
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0)
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(
+                           smem_u32(acc_empty))
+                       : "memory");
+      }
+      // c = c + alpha*T: lane = row, 32 consecutive rows per warp
+      const int i = mt * TC_BM + q * 32 + lane;
+      float *cp = c + i + (int64_t)m * (nt * TC_BN + h * 128);
+#pragma unroll 1
+      for (int cb = 0; cb < 128; cb += 32) {
+        float cv[32];
+#pragma unroll
+        for (int x = 0; x < 32; ++x) cv[x] = cp[(int64_t)m * (cb + x)];
+        uint32_t rt[32];
+        LFB_TMEM_LD16(tt + cb, rt);
+        LFB_TMEM_LD16(tt + cb + 16, rt + 16);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int x = 0; x < 32; ++x)
+          cp[(int64_t)m * (cb + x)] =
+              fadd(cv[x], fmul(alpha, __uint_as_float(rt[x])));
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(
+                     tmem),
+                 "r"(TC_TMEM_COLS)
+                 : "memory");
+  }
+}
+
+// }}}
+
 // {{{ prologue: tf32 hi/lo split (a transposed to K-major)
 
 __device__ __forceinline__ float rna_tf32(float x) {
@@ -370,7 +575,8 @@ bool sgemm_tc_shape_ok(int l, int m, int n) {
 
 // returns < 0 when the shape/workspace does not allow the tensor-core path
 int sgemm_tc(float alpha, const float *a, const float *b, float *c, int l,
-             int m, int n, float *ws, int64_t ws_floats, cudaStream_t s) {
+             int m, int n, float *ws, int64_t ws_floats, cudaStream_t s,
+             bool persistent) {
   if (!sgemm_tc_shape_ok(l, m, n) || !ws ||
       ws_floats < sgemm_tc_workspace_floats(l, m, n) || !aligned(ws, 16))
     return -1;
@@ -386,6 +592,27 @@ int sgemm_tc(float alpha, const float *a, const float *b, float *c, int l,
       !make_kmajor_map(&mbh, bhi, n, l, TC_BN) ||
       !make_kmajor_map(&mbl, blo, n, l, TC_BN))
     return fail(LFB_ERR_LAUNCH, "sgemm: tensor map encode failed");
+  if (persistent) {
+    cudaFuncSetAttribute(sgemm_tc2_kernel,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)TcSmem::total);
+    int sms = sm_count(nullptr);
+    if (sms <= 0) sms = 148;
+    const int tiles = (m / TC_BM) * (n / TC_BN);
+    sgemm_tc2_kernel<<<tiles < sms ? tiles : sms, TC2_THREADS, TcSmem::total,
+                       s>>>(mah, mal, mbh, mbl, alpha, c, l, m, n);
+    if (cudaPeekAtLastError() != cudaSuccess) {
+      cudaFuncAttributes fa{};
+      cudaFuncGetAttributes(&fa, sgemm_tc2_kernel);
+      cudaGetLastError();
+      return fail(LFB_ERR_LAUNCH,
+                  "lfb_sgemm_f32(tcgen05 persistent): launch failed "
+                  "(regs %d, max threads %d, local %zu, smem %zu)",
+                  fa.numRegs, fa.maxThreadsPerBlock, fa.localSizeBytes,
+                  (size_t)TcSmem::total);
+    }
+    return check_launch("lfb_sgemm_f32(tcgen05)");
+  }
   cudaFuncSetAttribute(sgemm_tc_kernel,
                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)TcSmem::total);

@@ -118,6 +118,121 @@ __global__ void __launch_bounds__(64, 1)
   if (i0 + lane < n) y[i0 + lane] = acc;
 }
 
+// {{{ split-j variant (geom->variant == 2): tolerance parity, HBM bound
+//
+// The reference's row chain s = (((0 + a(i,0)x(0)) + a(i,1)x(1)) + ...) is
+// n dependent DADDs; on B200 a dependent DADD costs ~18 cycles, so the bitwise
+// kernel above is bound by that chain (4096 x 18 cycles = 37 us at n = 4096,
+// profiles/r01_matvec.md), not by HBM.  This variant re-associates once:
+// W consumer warps per 32-row panel each run the reference chain over one
+// contiguous quarter of the columns (part 0 is bitwise the reference's
+// prefix), and y(i) = ((p0 + p1) + p2) + p3.  Within the north star's 1e-12
+// relative fp64 tolerance (tests: normwise), and the chains are W x shorter.
+constexpr int MVS_W = 4;       // consumer warps = column parts
+constexpr int MVS_STAGES = 3;  // ring depth per consumer warp
+
+struct MvsSmem {
+  static constexpr size_t tile_bytes = MV_ROWS * MV_JT * 8;  // 16 KB
+  static constexpr size_t x_bytes = MV_JT * 8;
+  static constexpr size_t nslot = (size_t)MVS_W * MVS_STAGES;
+  static constexpr size_t tiles_off = 1024;
+  static constexpr size_t xs_off = tiles_off + nslot * tile_bytes;
+  static constexpr size_t red_off = xs_off + nslot * x_bytes;
+  static constexpr size_t total = red_off + MVS_W * MV_ROWS * 8;
+};
+
+__global__ void __launch_bounds__(32 * (MVS_W + 1), 1)
+    matvec_split_kernel(const __grid_constant__ CUtensorMap tmap_a,
+                        double *__restrict__ y, const double *__restrict__ x,
+                        int n) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem);
+  uint64_t *empty = full + MvsSmem::nslot;
+  double *tiles = reinterpret_cast<double *>(smem + MvsSmem::tiles_off);
+  double *xs = reinterpret_cast<double *>(smem + MvsSmem::xs_off);
+  double *red = reinterpret_cast<double *>(smem + MvsSmem::red_off);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int i0 = blockIdx.x * MV_ROWS;
+  const int ntiles = (n + MV_JT - 1) / MV_JT;
+  // part w owns tiles [t0(w), t0(w + 1))
+  auto t0 = [&](int w) { return (int)(((int64_t)ntiles * w) / MVS_W); };
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < (int)MvsSmem::nslot; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (warp == MVS_W) {
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap_a) : "memory");
+      const uint64_t pol = policy_evict_first();
+      const int most = t0(MVS_W) - t0(MVS_W - 1);  // parts differ by <= 1
+      for (int q = 0; q < most + 1; ++q) {
+        for (int w = 0; w < MVS_W; ++w) {
+          const int tq = t0(w) + q;
+          if (tq >= t0(w + 1)) continue;
+          const int slot = w * MVS_STAGES + q % MVS_STAGES;
+          mbar_wait(&empty[slot], ((q / MVS_STAGES) & 1) ^ 1);
+          const int j0 = tq * MV_JT;
+          const int jn = min(MV_JT, n - j0);
+          const uint32_t xb = (uint32_t)jn * 8;
+          mbar_arrive_expect_tx(&full[slot], (uint32_t)MvsSmem::tile_bytes + xb);
+          asm volatile(
+              "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::"
+              "complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3}], [%4], "
+              "%5;" ::"r"(smem_u32(tiles + (size_t)slot * MV_ROWS * MV_JT)),
+              "l"(&tmap_a), "r"(i0), "r"(j0), "r"(smem_u32(&full[slot])),
+              "l"(pol)
+              : "memory");
+          bulk_g2s(xs + slot * MV_JT, x + j0, xb, &full[slot]);
+        }
+      }
+    }
+    return;
+  }
+
+  // consumer warp `warp`: the reference chain over its column part
+  double acc = 0.0;
+  const int nt = t0(warp + 1) - t0(warp);
+  for (int q = 0; q < nt; ++q) {
+    const int slot = warp * MVS_STAGES + q % MVS_STAGES;
+    mbar_wait(&full[slot], (q / MVS_STAGES) & 1);
+    const double *tile = tiles + (size_t)slot * MV_ROWS * MV_JT;
+    const double *xt = xs + slot * MV_JT;
+    const int jn = min(MV_JT, n - (t0(warp) + q) * MV_JT);
+    if (jn == MV_JT) {
+#pragma unroll 16
+      for (int jj = 0; jj < MV_JT; ++jj)
+        acc = dadd(acc, dmul(tile[jj * MV_ROWS + lane], xt[jj]));
+    } else {
+      for (int jj = 0; jj < jn; ++jj)
+        acc = dadd(acc, dmul(tile[jj * MV_ROWS + lane], xt[jj]));
+    }
+    __syncwarp();
+    if (lane == 0) {
+      fence_proxy_async_smem();
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(
+                       smem_u32(&empty[slot]))
+                   : "memory");
+    }
+  }
+  red[warp * MV_ROWS + lane] = acc;
+  named_bar_sync(1, 32 * MVS_W);
+  if (warp == 0) {
+    double s = red[lane];
+#pragma unroll
+    for (int w = 1; w < MVS_W; ++w) s = dadd(s, red[w * MV_ROWS + lane]);
+    if (i0 + lane < n) y[i0 + lane] = s;
+  }
+}
+
+// }}}
+
 // direct-load fallback: a warp per 32 rows, loads of a coalesced across lanes
 __global__ void matvec_direct_kernel(double *__restrict__ y,
                                      const double *__restrict__ a,
@@ -177,6 +292,14 @@ static int matvec_impl(double *y, const double *a, const double *x, int n,
       return fail(LFB_ERR_LAUNCH, "matvec: tensor map encode failed (%d)",
                   (int)r);
     const int grid = (n + MV_ROWS - 1) / MV_ROWS;
+    if (geom && geom->variant == 2 && n >= MVS_W * MV_JT) {
+      cudaFuncSetAttribute(matvec_split_kernel,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)MvsSmem::total);
+      matvec_split_kernel<<<grid, 32 * (MVS_W + 1), MvsSmem::total, s>>>(
+          tm, y, x, n);
+      return check_launch("lfb_matvec_f64");
+    }
     cudaFuncSetAttribute(matvec_tma_kernel,
                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)MvSmem::total);

@@ -570,7 +570,7 @@ static int launch_cpa(double *w, const double *u, const double *d,
 
 // (n, variant) -> kernel.  variant 0 is the tuned default per order.
 #define LFB_SEM_TABLE(S, A)                                                 \
-  S(8, 0, 4, 1, false, true, false)                                         \
+  S(8, 39, 4, 1, false, true, false)                                        \
   S(8, 1, 2, 3, false, false, false)                                        \
   S(8, 2, 4, 1, false, false, false)                                        \
   S(8, 3, 5, 1, false, false, false)                                        \
@@ -601,6 +601,12 @@ static int sem_dispatch(double *w, const double *u, const double *d,
 #define A(NN, VV, GG, PP, IL)                                               \
   if (n == NN && var == VV)                                                 \
     return launch_cpa<NN, GG, PP, IL>(w, u, d, g, nelt, geom, s, grid_out);
+  {
+    // d in the constant bank (semlap_kc.cu): the default for n = 8
+    const int rc = sem_kc_dispatch(n, var, w, u, d, g, nelt, geom, s,
+                                   grid_out);
+    if (rc != -1) return rc;
+  }
   LFB_SEM_TABLE(S, A)
 #undef S
 #undef A

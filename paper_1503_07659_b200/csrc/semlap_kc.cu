@@ -1,0 +1,333 @@
+// SEM Laplacian, even orders: d in the constant bank (BASELINE configs 3/4,
+// n = 8 default).
+//
+// Same reference arithmetic as semlap.cu (every * and +
+// rounded separately, l ascending, left-associative sums), so the result is
+// bitwise the reference's.
+//
+// Why a second n = 8 kernel: ncu on semlap_kernel (profiles/r01_sem65k.md)
+// shows the L1 LSU data pipe at 95 % of peak -- the kernel is bound by
+// shared-memory *instructions*, not bytes (bank reads 20 %).  Every warp-wide
+// LDS costs >= 2 wavefronts however few distinct addresses it touches, and a
+// third of them were broadcasts of d(k,.) / d(.,k) that are identical in all
+// lanes.  This kernel removes those and the other avoidable wavefronts:
+//  * d lives in a __constant__ slot; the unrolled loops index it with
+//    compile-time offsets, so d(k,l) is an immediate c[bank][offset] operand
+//    of the DMUL -- no load instruction at all.  The slot is filled by a
+//    stream-ordered device-to-device copy before the launch; a ring of
+//    SLOTS slots with one event each keeps launches on other streams from
+//    overwriting a slot a running kernel still reads (kc_acquire).
+//  * the per-thread d rows d(i,.), d(j,.) (phase 1) and d(.,i), d(.,j)
+//    (phase 2) are registers, loaded per phase from the constant slot;
+//  * u is transposed once per element into uT so the u(i,.,k) columns are
+//    16-byte pairs, and ws is stored transposed the same way (row stride
+//    N + 2: conflict-free for a half warp's 8 i values);
+//  * wr is stored unpadded (row stride N): a half warp's two j rows then
+//    fill the 16 double slots of a 128-byte line exactly, no conflict.
+// Everything else follows semlap_kernel: persistent CTAs of G groups of n^2
+// threads, thread (i,j) owns the k-column (i,j,*), u + g of a whole element
+// by bulk copies (TMA engine) into an SG-deep per-group ring.
+#include <mutex>
+
+#include "lfb_common.cuh"
+#include "semlap_common.cuh"
+
+namespace lfb {
+
+constexpr int KC_SLOTS = 4;
+constexpr int KC_MAXN2 = 16 * 16;
+
+__constant__ double c_dmat[KC_SLOTS][KC_MAXN2];  // d(a,b) at a + N b
+
+template <int N>
+struct KcCfg {
+  static constexpr int N2 = N * N;
+  static constexpr int NP = N * N * N;
+  static constexpr int T = ((N2 + 31) / 32) * 32;
+  static constexpr int R1 = N;      // wr row stride
+  static constexpr int R2 = N + 2;  // wsT / uT row stride
+  static constexpr int WR = N * N * N;
+  static constexpr int WS = R2 * N * N;
+  static constexpr int STAGE = 7 * NP;  // u then g
+};
+
+template <int N, int G, int SG>
+struct KcSmem {
+  using C = KcCfg<N>;
+  static constexpr size_t bars = 128;
+  static constexpr size_t scr_off = bars;
+  static constexpr size_t grp_scr = (size_t)(C::WR + 2 * C::WS);  // doubles
+  static constexpr size_t stage_off =
+      ((scr_off + (size_t)G * grp_scr * 8) + 127) / 128 * 128;
+  static constexpr size_t total = stage_off + (size_t)G * SG * C::STAGE * 8;
+};
+
+template <int SLOT, int N>
+__device__ __forceinline__ double cd(int a, int b) {
+  return c_dmat[SLOT][a + N * b];
+}
+
+template <int N, int G, int SG, int SLOT, bool SUMSQ>
+__global__ void __launch_bounds__(G *KcCfg<N>::T, 1)
+    semlap_kc_kernel(double *__restrict__ w, const double *__restrict__ u,
+                     const double *__restrict__ g, int64_t nelt,
+                     double *__restrict__ partials) {
+  using C = KcCfg<N>;
+  using L = KcSmem<N, G, SG>;
+  constexpr int NP = C::NP, T = C::T, R1 = C::R1, R2 = C::R2;
+  static_assert(G * SG <= 16, "too many stages");
+  static_assert(N % 2 == 0, "paired loads need even n");
+
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t *bars = reinterpret_cast<uint64_t *>(smem);
+  double *scr = reinterpret_cast<double *>(smem + L::scr_off);
+  double *stages = reinterpret_cast<double *>(smem + L::stage_off);
+
+  const int tid = threadIdx.x;
+  const int grp = tid / T;
+  const int lt = tid % T;
+  const int i = lt % N;
+  const int j = lt / N;
+  const bool active = lt < N * N;
+  // interleaved persistent order: concurrently streamed elements are adjacent
+  const int64_t ebase = blockIdx.x, estride = gridDim.x;
+  const int64_t count =
+      nelt > ebase ? (nelt - ebase + estride - 1) / estride : 0;
+
+  if (tid == 0) {
+    for (int s = 0; s < G * SG; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  const uint64_t pol = policy_evict_first();
+  auto issue = [&](int st, int64_t e) {
+    double *dst = stages + (size_t)st * C::STAGE;
+    mbar_arrive_expect_tx(&bars[st], (uint32_t)(C::STAGE * 8));
+    bulk_g2s_stream(dst, u + e * NP, NP * 8, &bars[st], pol);
+    bulk_g2s_stream(dst + NP, g + e * 6 * NP, 6 * NP * 8, &bars[st], pol);
+  };
+  if (lt == 0) {
+    for (int m = 0; m < SG; ++m) {
+      const int64_t t = grp + (int64_t)G * m;
+      if (t < count) issue(grp * SG + m, ebase + t * estride);
+    }
+  }
+
+
+  double *wr = scr + (size_t)grp * L::grp_scr;  // wr(i,j,k) @ i + N j + N^2 k
+  double *wsT = wr + C::WR;                     // ws(i,j,k) @ j + R2 i + R2 N k
+  double *uT = wsT + C::WS;                     // u (i,j,k) @ j + R2 i + R2 N k
+  double acc = 0.0;
+
+  for (int m = 0;; ++m) {
+    const int64_t t = grp + (int64_t)G * m;
+    if (t >= count) break;
+    const int64_t e = ebase + t * estride;
+    const int st = grp * SG + (m % SG);
+    mbar_wait(&bars[st], (uint32_t)((m / SG) & 1));
+    const double *su = stages + (size_t)st * C::STAGE;
+    const double *sg = su + NP;
+
+    double ucol[N], wt[N];
+    if (active) {
+#pragma unroll
+      for (int l = 0; l < N; ++l) ucol[l] = su[i + N * j + N * N * l];
+#pragma unroll
+      for (int k = 0; k < N; ++k) uT[j + R2 * i + R2 * N * k] = ucol[k];
+    }
+    named_bar_sync(1 + grp, T);  // uT complete
+
+    if (active) {
+      // per-thread d rows for phase 1 (constant-cache loads, no LSU traffic)
+      double d1a[N], d1b[N];
+#pragma unroll
+      for (int l = 0; l < N; ++l) {
+        d1a[l] = cd<SLOT, N>(i, l);  // d(i,l)
+        d1b[l] = cd<SLOT, N>(j, l);  // d(j,l)
+      }
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        double ur = 0.0, us = 0.0, ut = 0.0;
+        const double *row = su + N * j + N * N * k;    // u(.,j,k)
+        const double *col = uT + R2 * i + R2 * N * k;  // u(i,.,k)
+#pragma unroll
+        for (int l = 0; l < N; l += 2) {
+          const double2 r2 = *reinterpret_cast<const double2 *>(row + l);
+          const double2 c2 = *reinterpret_cast<const double2 *>(col + l);
+          ur = dadd(ur, dmul(d1a[l], r2.x));
+          us = dadd(us, dmul(d1b[l], c2.x));
+          ut = dadd(ut, dmul(cd<SLOT, N>(k, l), ucol[l]));
+          ur = dadd(ur, dmul(d1a[l + 1], r2.y));
+          us = dadd(us, dmul(d1b[l + 1], c2.y));
+          ut = dadd(ut, dmul(cd<SLOT, N>(k, l + 1), ucol[l + 1]));
+        }
+        const double2 *g2 =
+            reinterpret_cast<const double2 *>(sg + 6 * (i + N * j + N * N * k));
+        const double2 g01 = g2[0], g23 = g2[1], g45 = g2[2];
+        wr[i + N * j + N * N * k] =
+            dadd(dadd(dmul(g01.x, ur), dmul(g01.y, us)), dmul(g23.x, ut));
+        wsT[j + R2 * i + R2 * N * k] =
+            dadd(dadd(dmul(g01.y, ur), dmul(g23.y, us)), dmul(g45.x, ut));
+        wt[k] = dadd(dadd(dmul(g23.x, ur), dmul(g45.x, us)), dmul(g45.y, ut));
+      }
+    }
+    named_bar_sync(1 + grp, T);  // stage consumed, scratch complete
+
+    if (lt == 0) {
+      const int64_t tn = t + (int64_t)G * SG;
+      if (tn < count) {
+        fence_proxy_async_smem();
+        issue(st, ebase + tn * estride);
+      }
+    }
+
+    if (active) {
+      double d2a[N], d2b[N];
+#pragma unroll
+      for (int l = 0; l < N; ++l) {
+        d2a[l] = cd<SLOT, N>(l, i);  // d(l,i)
+        d2b[l] = cd<SLOT, N>(l, j);  // d(l,j)
+      }
+      double *we = w + e * NP + i + N * j;
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        const double *rr = wr + R1 * j + N * N * k;    // wr(.,j,k)
+        const double *rs = wsT + R2 * i + R2 * N * k;  // ws(i,.,k)
+        double s = 0.0;
+#pragma unroll
+        for (int l = 0; l < N; l += 2) {
+          const double2 r2 = *reinterpret_cast<const double2 *>(rr + l);
+          const double2 s2 = *reinterpret_cast<const double2 *>(rs + l);
+          s = dadd(dadd(dadd(s, dmul(d2a[l], r2.x)), dmul(d2b[l], s2.x)),
+                   dmul(cd<SLOT, N>(l, k), wt[l]));
+          s = dadd(dadd(dadd(s, dmul(d2a[l + 1], r2.y)),
+                        dmul(d2b[l + 1], s2.y)),
+                   dmul(cd<SLOT, N>(l + 1, k), wt[l + 1]));
+        }
+        we[N * N * k] = s;
+        if constexpr (SUMSQ) acc = dadd(acc, dmul(s, s));
+      }
+    }
+    named_bar_sync(1 + grp, T);  // scratch reads done before the next element
+  }
+
+  if constexpr (SUMSQ) block_sumsq_partial(acc, partials);
+}
+
+// {{{ constant-slot ring
+
+struct KcRing {
+  std::mutex mu;
+  int next = 0;
+  cudaEvent_t ev[KC_SLOTS] = {};
+  bool used[KC_SLOTS] = {};
+};
+
+static KcRing &kc_ring(int dev) {
+  static KcRing rings[64];
+  return rings[dev & 63];
+}
+
+// Copy d (n*n doubles, device memory) into a free constant slot on `s`,
+// ordered after the last kernel that read that slot (on any stream).  The
+// caller launches on `s` and then calls kc_release.
+static int kc_acquire(const double *d, int n, cudaStream_t s, int *slot,
+                      std::unique_lock<std::mutex> *lk) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess)
+    return fail(LFB_ERR_LAUNCH, "semlap: cudaGetDevice failed");
+  KcRing &r = kc_ring(dev);
+  *lk = std::unique_lock<std::mutex>(r.mu);
+  const int k = r.next;
+  r.next = (r.next + 1) % KC_SLOTS;
+  if (!r.ev[k] &&
+      cudaEventCreateWithFlags(&r.ev[k], cudaEventDisableTiming) != cudaSuccess)
+    return fail(LFB_ERR_LAUNCH, "semlap: event create failed");
+  if (r.used[k]) cudaStreamWaitEvent(s, r.ev[k], 0);
+  if (cudaMemcpyToSymbolAsync(c_dmat, d, (size_t)n * n * 8,
+                              (size_t)k * KC_MAXN2 * 8,
+                              cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+    return fail(LFB_ERR_LAUNCH, "semlap: copy of d to the constant bank failed");
+  *slot = k;
+  return LFB_OK;
+}
+
+static void kc_release(int slot, cudaStream_t s) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  KcRing &r = kc_ring(dev);  // caller still holds r.mu
+  cudaEventRecord(r.ev[slot], s);
+  r.used[slot] = true;
+}
+
+// }}}
+
+template <int N, int G, int SG, int SLOT>
+static void kc_launch_slot(bool sumsq, int grid, size_t smem, double *w,
+                           const double *u, const double *g, int64_t nelt,
+                           double *partials, cudaStream_t s) {
+  auto k = sumsq ? semlap_kc_kernel<N, G, SG, SLOT, true>
+                 : semlap_kc_kernel<N, G, SG, SLOT, false>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)smem);
+  k<<<grid, G * KcCfg<N>::T, smem, s>>>(w, u, g, nelt, partials);
+}
+
+template <int N, int G, int SG>
+static int launch_kc(double *w, const double *u, const double *d,
+                     const double *g, int64_t nelt, const lfb_launch *geom,
+                     cudaStream_t s, int64_t *grid_out) {
+  using L = KcSmem<N, G, SG>;
+  static_assert(L::total <= 227 * 1024, "smem");
+  static_assert(N * N <= KC_MAXN2, "constant slot");
+  int sms = sm_count(geom);
+  if (sms <= 0) sms = 148;
+  const int per_sm = (geom && geom->ctas_per_sm > 0) ? geom->ctas_per_sm : 1;
+  int64_t grid64 = (int64_t)sms * per_sm;
+  if (grid64 * G > nelt) grid64 = (nelt + G - 1) / G;
+  const int grid = (int)(grid64 < 1 ? 1 : grid64);
+  if (grid_out) {
+    *grid_out = grid;
+    return LFB_OK;
+  }
+  const bool sumsq = geom && geom->sumsq;
+  if (sumsq && (!geom->workspace || geom->workspace_len < grid))
+    return fail(LFB_ERR_ARG, "semlap: sumsq workspace too small");
+  double *part = sumsq ? geom->workspace : nullptr;
+  int slot = 0;
+  std::unique_lock<std::mutex> lk;
+  if (int rc = kc_acquire(d, N, s, &slot, &lk)) return rc;
+  switch (slot) {
+    case 0: kc_launch_slot<N, G, SG, 0>(sumsq, grid, L::total, w, u, g, nelt, part, s); break;
+    case 1: kc_launch_slot<N, G, SG, 1>(sumsq, grid, L::total, w, u, g, nelt, part, s); break;
+    case 2: kc_launch_slot<N, G, SG, 2>(sumsq, grid, L::total, w, u, g, nelt, part, s); break;
+    default: kc_launch_slot<N, G, SG, 3>(sumsq, grid, L::total, w, u, g, nelt, part, s); break;
+  }
+  kc_release(slot, s);
+  lk.unlock();
+  if (int rc = check_launch("lfb_semlap_f64")) return rc;
+  return sumsq ? sem_sumsq_finish(geom->workspace, grid, geom->sumsq, s)
+               : LFB_OK;
+}
+
+// (n, variant) -> (G, SG).  -1: no constant-bank entry.
+#define LFB_KC_TABLE(X) \
+  X(8, 0, 4, 1)         \
+  X(8, 40, 4, 1)        \
+  X(8, 41, 5, 1)        \
+  X(8, 42, 3, 2)
+
+int sem_kc_dispatch(int n, int variant, double *w, const double *u,
+                    const double *d, const double *g, int64_t nelt,
+                    const lfb_launch *geom, cudaStream_t s,
+                    int64_t *grid_out) {
+#define X(NN, VV, GG, SS)                                                   \
+  if (n == NN && variant == VV)                                             \
+    return launch_kc<NN, GG, SS>(w, u, d, g, nelt, geom, s, grid_out);
+  LFB_KC_TABLE(X)
+#undef X
+  return -1;
+}
+
+}  // namespace lfb

@@ -64,6 +64,40 @@ __global__ void fill_vec_kernel(T *__restrict__ out, T a, int64_t nvec) {
     __stcs(o + q, v);
 }
 
+// fill through the TMA engine: a CTA writes `a` into a CHUNK-byte smem tile
+// once, then one thread streams that tile to its share of the output with
+// bulk shared->global copies (cp.async.bulk ... bulk_group).  No per-element
+// store instructions at all; the copies only read smem, so the tile is reused
+// for every chunk and the CTA waits for the reads before it exits.
+constexpr int FILL_CHUNK = 32768;
+
+template <typename T>
+__global__ void __launch_bounds__(256, 1)
+    fill_bulk_kernel(T *__restrict__ out, T a, int64_t nbytes) {
+  extern __shared__ __align__(128) unsigned char fsmem[];
+  T *tile = reinterpret_cast<T *>(fsmem);
+  for (int q = threadIdx.x; q < FILL_CHUNK / (int)sizeof(T); q += blockDim.x)
+    tile[q] = a;
+  fence_proxy_async_smem();  // generic-proxy writes -> async-proxy reads
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int64_t nchunks = (nbytes + FILL_CHUNK - 1) / FILL_CHUNK;
+    unsigned char *o = reinterpret_cast<unsigned char *>(out);
+    for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+      const int64_t off = c * FILL_CHUNK;
+      const int64_t rem = nbytes - off;
+      const uint32_t bytes = (uint32_t)(rem < FILL_CHUNK ? rem : FILL_CHUNK);
+      asm volatile(
+          "cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(
+              o + off),
+          "r"(smem_u32(tile)), "r"(bytes)
+          : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+  }
+}
+
 template <typename T>
 __global__ void fill_scalar_kernel(T *__restrict__ out, T a, int64_t n) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -163,9 +197,22 @@ static int fill_impl(const char *what, T *out, T a, int n,
   constexpr int W = Vec<T>::W;
   if (aligned(out, 16)) {
     int64_t nvec = n / W;
-    if (nvec)
+    const bool bulk = !(geom && geom->variant == 1);
+    if (nvec && bulk) {
+      // whole 16-byte vectors by bulk copies, one CTA per SM
+      int sms = sm_count(geom);
+      if (sms <= 0) sms = 148;
+      const int64_t nbytes = nvec * 16;
+      const int64_t chunks = (nbytes + FILL_CHUNK - 1) / FILL_CHUNK;
+      const int grid = (int)(chunks < sms ? chunks : sms);
+      cudaFuncSetAttribute(fill_bulk_kernel<T>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           FILL_CHUNK);
+      fill_bulk_kernel<T><<<grid, 256, FILL_CHUNK, s>>>(out, a, nbytes);
+    } else if (nvec) {
       fill_vec_kernel<T><<<grid_for(nvec, block, geom, 4), block, 0, s>>>(
           out, a, nvec);
+    }
     int64_t done = nvec * W;
     if (done < n)
       fill_scalar_kernel<T><<<1, 32, 0, s>>>(out + done, a, n - done);

@@ -101,7 +101,7 @@ def test_semlap_o7_65536_elements(cuda):
                [(0, 1024), (30000, 31000), (nelt - 1024, nelt)])
 
 
-@pytest.mark.parametrize("variant", [1, 2, 3, 4, 5, 6, 7, 9, 10, 11, 12, 13, 14, 15, 16, 17, 18, 19])
+@pytest.mark.parametrize("variant", [1, 2, 3, 4, 5, 6, 7, 9, 10, 11, 12, 13, 14, 15, 16, 17, 18, 19, 39, 40, 41, 42])
 def test_semlap_o7_variants(cuda, variant):
     nelt = 4096
     _sem_check(8, nelt, fx.semlap_source(8), cuda, [(0, nelt)],
@@ -170,6 +170,34 @@ def test_semlap_ragged_and_guarded(cuda, block, nelt):
     _sem_check(8, nelt, src, cuda, [(0, nelt)], seed=block)
 
 
+def test_semlap_constant_d_slots_across_streams(cuda):
+    """The n = 8 default keeps d in a ring of constant-bank slots: launches
+    with different d on two streams, more launches than slots, each result
+    bitwise the oracle's (no slot overwritten while a kernel reads it)."""
+    n, nelt = 8, 2048
+    _raw, knl = fx.translate(fx.semlap_source(n))
+    streams = [torch.cuda.Stream(cuda), torch.cuda.Stream(cuda)]
+    cases = []
+    for c in range(6):
+        u, d, g = _sem_inputs(n, nelt, cuda, 100 + c)
+        w = torch.full_like(u, float("nan"))
+        env = lfb.env_from_buffers(knl, {"nelt": nelt},
+                                   {"u": u, "d": d, "g": g, "w": w})
+        cases.append((env, u, d, g, w))
+    for s in streams:
+        s.wait_stream(torch.cuda.current_stream(cuda))
+    for rep in range(3):
+        for c, (env, *_rest) in enumerate(cases):
+            s = streams[c % 2]
+            with torch.cuda.stream(s):
+                lfb.Launcher(knl, env).launch(stream=s.cuda_stream)
+    torch.cuda.synchronize()
+    for env, u, d, g, w in cases:
+        ref = oracle.semlap(np.zeros(nelt * n ** 3), u.cpu().numpy(),
+                            d.cpu().numpy(), g.cpu().numpy(), n, nelt)
+        assert w.cpu().numpy().tobytes() == ref.tobytes()
+
+
 @pytest.mark.parametrize("n", [8, 5])
 def test_semlap_sumsq_epilogue(cuda, n):
     _raw, knl = fx.translate(fx.semlap_source(n))
@@ -224,6 +252,21 @@ def test_fill_axpy_ragged(cuda, n):
         assert (out.arrays["out"].data.cpu().numpy() == npt(0.1)).all()
 
 
+@pytest.mark.parametrize("n", [1 << 20, (1 << 20) + 2, 1000003, 4097])
+@pytest.mark.parametrize("variant", [0, 1])
+def test_fill_no_overrun(cuda, n, variant):
+    """The bulk-copy fill (variant 0) and the vector-store fill (variant 1)
+    write exactly out[0, n): a canary after the end stays untouched."""
+    for dt, tdt in (("f64", torch.float64), ("f32", torch.float32)):
+        _r, kf = fx.translate(fx.fill_source(dt))
+        base = torch.zeros(n + 64, dtype=tdt, device=cuda)
+        env = lfb.env_from_buffers(kf, {"n": n}, {"out": base[:n]},
+                                   {"a": 0.75})
+        lfb.interpret(kf, env, inplace=True, variant=variant)
+        h = base.cpu().numpy()
+        assert (h[:n] == 0.75).all() and (h[n:] == 0).all()
+
+
 def test_fill_misaligned_pointer(cuda):
     _r, kf = fx.translate(fx.fill_source("f64"))
     base = torch.zeros(1001, dtype=torch.float64, device=cuda)
@@ -247,6 +290,32 @@ def test_matvec(cuda, n):
     ref = oracle.matvec(np.zeros(n), a.cpu().numpy(), x.cpu().numpy(), n,
                         threads=8)
     assert y.cpu().numpy().tobytes() == ref.tobytes()
+
+
+@pytest.mark.parametrize("n", [4096, 256, 1024 + 128, 1000, 2050])
+def test_matvec_split_j(cuda, n):
+    """variant=2: W column parts per row, summed in part order -- tolerance
+    parity (north star: 1e-12 relative for fp64), here normwise and per row
+    on [-1, 1) data like make_env's."""
+    raw, knl = fx.translate(fx.matvec_source("f64", script=n % 128 == 0))
+    knl = knl if n % 128 == 0 else raw
+    gen = torch.Generator(device=cuda).manual_seed(n + 1)
+    a = torch.rand(n * n, dtype=torch.float64, device=cuda, generator=gen)
+    x = torch.rand(n, dtype=torch.float64, device=cuda, generator=gen)
+    a = a * 2 - 1
+    x = x * 2 - 1
+    y = torch.full((n,), float("nan"), dtype=torch.float64, device=cuda)
+    env = lfb.env_from_buffers(knl, {"n": n}, {"a": a, "x": x, "y": y})
+    lfb.interpret(knl, env, inplace=True, variant=2)
+    ah, xh = a.cpu().numpy(), x.cpu().numpy()
+    ref = oracle.matvec(np.zeros(n), ah, xh, n, threads=8)
+    got = y.cpu().numpy()
+    assert np.isfinite(got).all()
+    err = np.abs(got - ref)
+    assert err.max() <= 1e-12 * np.abs(ref).max()
+    # per row against the magnitude the row sums over
+    scale = np.abs(ah.reshape(n, n).T) @ np.abs(xh)
+    assert (err <= 1e-12 * scale).all()
 
 
 @pytest.mark.parametrize("n", [97, 130, 4095])
@@ -318,10 +387,13 @@ def test_wrong_shape_input_is_interp_error(cuda):
 
 # {{{ sgemm on tensor cores (tolerance parity)
 
+@pytest.mark.parametrize("variant", [2, 3])
 @pytest.mark.parametrize("m,n,l", [(128, 256, 32), (256, 512, 256),
-                                   (1024, 768, 4096), (384, 256, 8192)])
-def test_sgemm_tensor_cores(cuda, m, n, l):
-    """variant=2: tcgen05 kind::tf32 with the 3xTF32 split.  Tolerance
+                                   (1024, 768, 4096), (384, 256, 8192),
+                                   (3200, 3072, 64), (4096, 2048, 512)])
+def test_sgemm_tensor_cores(cuda, m, n, l, variant):
+    """variant=2: tcgen05 kind::tf32 with the 3xTF32 split (persistent,
+    double-buffered TMEM; variant 3 the first one-tile-per-CTA kernel).  Tolerance
     (north star: 1e-5 relative for fp32), normwise against the reference's
     own fp32 sequential result (the oracle), and the same bound against an
     exact fp64 product; the reference's own rounding error is printed."""
@@ -335,7 +407,7 @@ def test_sgemm_tensor_cores(cuda, m, n, l):
         knl, {"m": m, "n": n, "l": l},
         {"a": torch.from_numpy(a).to(cuda), "b": torch.from_numpy(b).to(cuda),
          "c": torch.from_numpy(c.copy()).to(cuda)}, {"alpha": alpha})
-    out = lfb.interpret(knl, env, variant=2)
+    out = lfb.interpret(knl, env, variant=variant)
     got = out.arrays["c"].data.cpu().numpy().astype(np.float64)
     ref = oracle.sgemm(alpha, a, b, c.copy(), l, m, n, threads=8) \
         .astype(np.float64)

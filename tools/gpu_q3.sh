@@ -1,0 +1,8 @@
+#!/bin/bash
+cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -q -rf -p no:cacheprovider -k "sgemm" > gpurun_out/pytest_q3.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_q3.log
+for v in 0 3; do timeout 300 python bench.py --workload sgemm --variant $v --steps 5 > gpurun_out/bench_sgemm_v$v.json 2>>gpurun_out/q3.err; done
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:sgemm_tc2 -s 1 -c 1 -o gpurun_out/prof_sgemm2 python bench.py --workload sgemm --steps 1 --warmup 3 > gpurun_out/ncu_sgemm2.log 2>&1
+timeout 300 python bench.py --workload matvec > gpurun_out/bench_matvec.json 2>>gpurun_out/q3.err
+timeout 300 python bench.py --workload fill > gpurun_out/bench_fill.json 2>>gpurun_out/q3.err
+timeout 300 python bench.py --workload axpy > gpurun_out/bench_axpy.json 2>>gpurun_out/q3.err
