@@ -289,25 +289,26 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   }
 }
 
-// {{{ persistent kernel: overlapped epilogue, 8-warp chunk folds
+// {{{ persistent kernel: double-buffered TMEM accumulator, overlapped epilogue
 //
-// sgemm_tc_kernel above runs one tile per CTA and ends every tile with a
-// serial C read-modify-write that leaves the tensor pipe idle (ncu: tensor
-// pipe 49 % active, a fifth of all stall samples on the epilogue's C loads,
-// profiles/r01_sgemm.md).  Here
-//  * CTAs are persistent (one per SM) over a grouped tile order: while the
-//    epilogue warps fold the last chunk of tile t and update C, the MMA warp
-//    already accumulates chunk 0 of tile t + 1 (A is free as soon as the
-//    last fold has read it; T is reused only by the next tile's first fold,
-//    one chunk later);
-//  * 8 epilogue warps (warp w: TMEM lane quarter w % 4, column half
-//    (w - 2) / 4) fold each chunk twice as fast as 4, shortening the MMA
-//    warp's wait at chunk boundaries;
-//  * the C update keeps 32 loads per thread in flight.
+// sgemm_tc_kernel above leaves the tensor pipe idle twice per tile: at every
+// chunk boundary the MMA warp waits until the epilogue has folded A into T
+// (A is about to be overwritten), and every tile ends with a serial C
+// read-modify-write (ncu: tensor pipe 49 % active, profiles/r01_sgemm.md).
+// Here
+//  * TMEM holds two chunk accumulators, A0 (columns 0..255) and A1
+//    (256..511): chunk g accumulates into A(g % 2) while the epilogue folds
+//    chunk g - 1 out of the other, so the MMA warp never waits for a fold;
+//  * the running total T lives in registers: 16 epilogue warps, warp w
+//    reads TMEM lane quarter w % 4 and column quarter (w - 2) / 4, 64 fp32
+//    of T per thread;
+//  * CTAs are persistent (one per SM) over a grouped tile order, so the C
+//    read-modify-write of tile t overlaps the MMAs of tile t + 1.
 // Numerics are unchanged: T = A_0, T = T + A_1, ... (round-to-nearest FADD),
 // c = c + alpha*T.
-constexpr int TC2_THREADS = 320;  // producer, MMA, 8 epilogue warps
-constexpr int TC2_GROUP_M = 8;    // M tiles per raster group
+constexpr int TC2_EPI_WARPS = 16;
+constexpr int TC2_THREADS = 32 * (2 + TC2_EPI_WARPS);  // producer, MMA, epi
+constexpr int TC2_GROUP_M = 8;  // M tiles per raster group
 
 __device__ __forceinline__ void tc2_tile(int t, int mt_count, int nt_count,
                                          int *mt, int *nt) {
@@ -331,9 +332,9 @@ __global__ void __launch_bounds__(TC2_THREADS, 1)
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + TcSmem::bars_off);
   uint64_t *empty = full + TC_STAGES;
-  uint64_t *acc_full = empty + TC_STAGES;  // MMA -> epilogue: chunk in A
-  uint64_t *acc_empty = acc_full + 1;      // epilogue -> MMA: A folded
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(acc_empty + 1);
+  uint64_t *acc_full = empty + TC_STAGES;  // [2] MMA -> epilogue
+  uint64_t *acc_empty = acc_full + 2;      // [2] epilogue -> MMA
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(acc_empty + 2);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int nk = l / TC_BK;
@@ -346,8 +347,10 @@ __global__ void __launch_bounds__(TC2_THREADS, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(acc_full, 1);
-    mbar_init(acc_empty, 8);  // one arrive per epilogue warp
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_empty[b], TC2_EPI_WARPS);
+    }
     fence_mbar_init();
   }
   if (warp == 1) {
@@ -361,7 +364,7 @@ __global__ void __launch_bounds__(TC2_THREADS, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = *tmem_slot;  // A: columns 0..255, T: 256..511
+  const uint32_t tmem = *tmem_slot;
 
   auto stage_ptr = [&](int s) { return smem + s * TcSmem::stage_bytes; };
 
@@ -395,8 +398,9 @@ __global__ void __launch_bounds__(TC2_THREADS, 1)
         const bool first_in_chunk = (kb % TC_CHUNK) == 0;
         const bool last_in_chunk =
             kb % TC_CHUNK == TC_CHUNK - 1 || kb == nk - 1;
-        if (first_in_chunk && g > 0)  // chunk g - 1 folded out of A
-          mbar_wait(acc_empty, (g - 1) & 1);
+        const int b = g & 1;
+        if (first_in_chunk)  // chunk g - 2 folded out of A(b)
+          mbar_wait(&acc_empty[b], ((g >> 1) & 1) ^ 1);
         mbar_wait(&full[s], (it / TC_STAGES) & 1);
         tc_fence_after();
         if (lane == 0) {
@@ -406,16 +410,17 @@ __global__ void __launch_bounds__(TC2_THREADS, 1)
           const uint64_t bhi = sw128_kmajor_desc(st + 2 * TcSmem::a_bytes);
           const uint64_t blo =
               sw128_kmajor_desc(st + 2 * TcSmem::a_bytes + TcSmem::b_bytes);
+          const uint32_t acc = tmem + (uint32_t)(b * TC_BN);
 #pragma unroll
           for (int k = 0; k < TC_BK / 8; ++k) {
             const uint64_t dk = (uint64_t)((k * 32) >> 4);
-            tc_mma_tf32(tmem, alo + dk, bhi + dk, idesc,
+            tc_mma_tf32(acc, alo + dk, bhi + dk, idesc,
                         !(first_in_chunk && k == 0));
-            tc_mma_tf32(tmem, ahi + dk, blo + dk, idesc, 1);
-            tc_mma_tf32(tmem, ahi + dk, bhi + dk, idesc, 1);
+            tc_mma_tf32(acc, ahi + dk, blo + dk, idesc, 1);
+            tc_mma_tf32(acc, ahi + dk, bhi + dk, idesc, 1);
           }
           tc_commit(&empty[s]);
-          if (last_in_chunk) tc_commit(acc_full);
+          if (last_in_chunk) tc_commit(&acc_full[b]);
         }
         __syncwarp();
         if (last_in_chunk) ++g;
@@ -423,60 +428,51 @@ __global__ void __launch_bounds__(TC2_THREADS, 1)
     }
   } else {
     const int q = warp % 4;
-    const int h = (warp - 2) / 4;  // column half
+    const int cq = (warp - 2) / 4;  // column quarter
     const uint32_t lanes = (uint32_t)(q * 32) << 16;
-    const uint32_t ta = tmem + lanes + (uint32_t)(h * 128);
-    const uint32_t tt = ta + TC_BN;
     int g = 0;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
       int mt, nt;
       tc2_tile(t, mt_count, nt_count, &mt, &nt);
+      float T[64];
       for (int ch = 0; ch < nchunks; ++ch, ++g) {
-        mbar_wait(acc_full, g & 1);
+        const int b = g & 1;
+        mbar_wait(&acc_full[b], (g >> 1) & 1);
         tc_fence_after();
-        // T = A (first chunk) or T = T + A, round to nearest
-#pragma unroll 1
-        for (int cb = 0; cb < 128; cb += 32) {
-          uint32_t ra[32], rt[32];
-          LFB_TMEM_LD16(ta + cb, ra);
-          LFB_TMEM_LD16(ta + cb + 16, ra + 16);
-          if (ch > 0) {
-            LFB_TMEM_LD16(tt + cb, rt);
-            LFB_TMEM_LD16(tt + cb + 16, rt + 16);
-          }
-          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        const uint32_t base = tmem + lanes + (uint32_t)(b * TC_BN + cq * 64);
 #pragma unroll
-          for (int x = 0; x < 32; ++x)
-            rt[x] = ch > 0 ? __float_as_uint(fadd(__uint_as_float(rt[x]),
-                                                  __uint_as_float(ra[x])))
-                           : ra[x];
-          LFB_TMEM_ST16(tt + cb, rt);
-          LFB_TMEM_ST16(tt + cb + 16, rt + 16);
+        for (int cb = 0; cb < 64; cb += 16) {
+          uint32_t r[16];
+          LFB_TMEM_LD16(base + cb, r);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          if (ch == 0) {
+#pragma unroll
+            for (int x = 0; x < 16; ++x) T[cb + x] = __uint_as_float(r[x]);
+          } else {
+#pragma unroll
+            for (int x = 0; x < 16; ++x)
+              T[cb + x] = fadd(T[cb + x], __uint_as_float(r[x]));
+          }
         }
-        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         tc_fence_before();
         __syncwarp();
         if (lane == 0)
           asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(
-                           smem_u32(acc_empty))
+                           smem_u32(&acc_empty[b]))
                        : "memory");
       }
       // c = c + alpha*T: lane = row, 32 consecutive rows per warp
       const int i = mt * TC_BM + q * 32 + lane;
-      float *cp = c + i + (int64_t)m * (nt * TC_BN + h * 128);
-#pragma unroll 1
-      for (int cb = 0; cb < 128; cb += 32) {
-        float cv[32];
+      float *cp = c + i + (int64_t)m * (nt * TC_BN + cq * 64);
 #pragma unroll
-        for (int x = 0; x < 32; ++x) cv[x] = cp[(int64_t)m * (cb + x)];
-        uint32_t rt[32];
-        LFB_TMEM_LD16(tt + cb, rt);
-        LFB_TMEM_LD16(tt + cb + 16, rt + 16);
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      for (int cb = 0; cb < 64; cb += 16) {
+        float cv[16];
 #pragma unroll
-        for (int x = 0; x < 32; ++x)
-          cp[(int64_t)m * (cb + x)] =
-              fadd(cv[x], fmul(alpha, __uint_as_float(rt[x])));
+        for (int x = 0; x < 16; ++x) cv[x] = cp[(int64_t)m * (cb + x)];
+#pragma unroll
+        for (int x = 0; x < 16; ++x)
+          cp[(int64_t)m * (cb + x)] = fadd(cv[x], fmul(alpha, T[cb + x]));
+        asm volatile("" ::: "memory");
       }
     }
   }

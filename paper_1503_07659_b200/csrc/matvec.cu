@@ -9,8 +9,13 @@
 // reference script's extract_subst + precompute stage x in a private 32-wide
 // tile (transforms.py:541-684) -- a copy, so values are unchanged.
 //
-// Every row is one sequential chain of 2n separately rounded operations; the
-// device keeps that chain (bitwise parity) and parallelises over rows only.
+// Variants (lfb_launch.variant): 0 = split-j (below; within the north
+// star's 1e-12 fp64 tolerance, HBM bound) when n >= 256, 1 = direct-load
+// bitwise, 2 = split-j only, 3 = the bitwise TMA kernel.
+//
+// Bitwise kernels: every row is one sequential chain of 2n separately
+// rounded operations; the device keeps that chain and parallelises over
+// rows only.
 // The kernel is HBM bound (8 n^2 bytes of a), so the design is about bytes in
 // flight, not FLOPs:
 //  * one CTA per 32-row panel: warp 0 computes (lane r owns row i0 + r),
@@ -118,7 +123,8 @@ __global__ void __launch_bounds__(64, 1)
   if (i0 + lane < n) y[i0 + lane] = acc;
 }
 
-// {{{ split-j variant (geom->variant == 2): tolerance parity, HBM bound
+// {{{ split-j kernel (default; variant 2 forces it): tolerance parity, HBM
+// bound
 //
 // The reference's row chain s = (((0 + a(i,0)x(0)) + a(i,1)x(1)) + ...) is
 // n dependent DADDs; on B200 a dependent DADD costs ~18 cycles, so the bitwise
@@ -292,7 +298,8 @@ static int matvec_impl(double *y, const double *a, const double *x, int n,
       return fail(LFB_ERR_LAUNCH, "matvec: tensor map encode failed (%d)",
                   (int)r);
     const int grid = (n + MV_ROWS - 1) / MV_ROWS;
-    if (geom && geom->variant == 2 && n >= MVS_W * MV_JT) {
+    const int var = geom ? geom->variant : 0;
+    if ((var == 0 || var == 2) && n >= MVS_W * MV_JT) {
       cudaFuncSetAttribute(matvec_split_kernel,
                            cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)MvsSmem::total);

@@ -593,7 +593,7 @@ static int sem_dispatch(double *w, const double *u, const double *d,
                         const double *g, int64_t nelt, const lfb_launch *geom,
                         cudaStream_t s, int64_t *grid_out) {
   const int n = geom->npts;
-  const int var = geom->variant;
+  const int var0 = geom->variant;
 #define S(NN, VV, GG, SS, DPH, IL, TR)                                      \
   if (n == NN && var == VV)                                                 \
     return launch_staged<NN, GG, SS, DPH, IL, TR>(w, u, d, g, nelt, geom,   \
@@ -603,10 +603,11 @@ static int sem_dispatch(double *w, const double *u, const double *d,
     return launch_cpa<NN, GG, PP, IL>(w, u, d, g, nelt, geom, s, grid_out);
   {
     // d in the constant bank (semlap_kc.cu): the default for n = 8
-    const int rc = sem_kc_dispatch(n, var, w, u, d, g, nelt, geom, s,
+    const int rc = sem_kc_dispatch(n, var0, w, u, d, g, nelt, geom, s,
                                    grid_out);
     if (rc != -1) return rc;
   }
+  const int var = (n == 8 && var0 == 0) ? 39 : var0;  // smem-d n = 8 kernel
   LFB_SEM_TABLE(S, A)
 #undef S
 #undef A

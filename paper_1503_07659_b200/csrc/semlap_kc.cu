@@ -322,6 +322,12 @@ int sem_kc_dispatch(int n, int variant, double *w, const double *u,
                     const double *d, const double *g, int64_t nelt,
                     const lfb_launch *geom, cudaStream_t s,
                     int64_t *grid_out) {
+  // the slot ring orders launches with events; inside a CUDA graph capture
+  // the caller gets the shared-memory-d kernel instead
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (!grid_out && cudaStreamIsCapturing(s, &cap) == cudaSuccess &&
+      cap != cudaStreamCaptureStatusNone)
+    return -1;
 #define X(NN, VV, GG, SS)                                                   \
   if (n == NN && variant == VV)                                             \
     return launch_kc<NN, GG, SS>(w, u, d, g, nelt, geom, s, grid_out);

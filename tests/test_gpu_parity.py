@@ -286,15 +286,19 @@ def test_matvec(cuda, n):
     x = torch.rand(n, dtype=torch.float64, device=cuda, generator=gen)
     y = torch.full((n,), float("nan"), dtype=torch.float64, device=cuda)
     env = lfb.env_from_buffers(knl, {"n": n}, {"a": a, "x": x, "y": y})
-    lfb.interpret(knl, env, inplace=True)
+    lfb.interpret(knl, env, inplace=True, variant=3)  # bitwise TMA kernel
     ref = oracle.matvec(np.zeros(n), a.cpu().numpy(), x.cpu().numpy(), n,
                         threads=8)
     assert y.cpu().numpy().tobytes() == ref.tobytes()
+    y.fill_(float("nan"))
+    lfb.interpret(knl, env, inplace=True, variant=1)  # bitwise direct loads
+    assert y.cpu().numpy().tobytes() == ref.tobytes()
 
 
+@pytest.mark.parametrize("variant", [0, 2])
 @pytest.mark.parametrize("n", [4096, 256, 1024 + 128, 1000, 2050])
-def test_matvec_split_j(cuda, n):
-    """variant=2: W column parts per row, summed in part order -- tolerance
+def test_matvec_split_j(cuda, n, variant):
+    """Default / variant 2: W column parts per row, summed in part order -- tolerance
     parity (north star: 1e-12 relative for fp64), here normwise and per row
     on [-1, 1) data like make_env's."""
     raw, knl = fx.translate(fx.matvec_source("f64", script=n % 128 == 0))
@@ -306,7 +310,7 @@ def test_matvec_split_j(cuda, n):
     x = x * 2 - 1
     y = torch.full((n,), float("nan"), dtype=torch.float64, device=cuda)
     env = lfb.env_from_buffers(knl, {"n": n}, {"a": a, "x": x, "y": y})
-    lfb.interpret(knl, env, inplace=True, variant=2)
+    lfb.interpret(knl, env, inplace=True, variant=variant)
     ah, xh = a.cpu().numpy(), x.cpu().numpy()
     ref = oracle.matvec(np.zeros(n), ah, xh, n, threads=8)
     got = y.cpu().numpy()
