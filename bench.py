@@ -280,7 +280,8 @@ def sem_bench(args, rank, world, local):
                      "traffic": _traffic(f"semlap_n{n}"),
                      "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": bytes_per_launch,
-                     "kernel": "semlap_kernel (1 launch per step)",
+                     "kernel": "semlap_kc_kernel (1 launch per step, after "
+                               "a 512 B d -> constant-bank copy)",
                      "stream_probe_gbs": probe_gbs,
                      "stream_probe_note": "same buffers, same bytes, no "
                                           "arithmetic (lfb_probe_stream)"},
@@ -325,6 +326,7 @@ def sem_e2e(knl, n, nelt, dev, steps, chunk=1 << 17):
                                       device=dev)})
     chunks = [(s, min(nelt, s + chunk)) for s in range(0, nelt, chunk)]
     launches = [0]
+    resident = {}  # mode "resident": g and d uploaded once, kept on device
 
     def step():
         for c, (e0, e1) in enumerate(chunks):
@@ -333,12 +335,17 @@ def sem_e2e(knl, n, nelt, dev, steps, chunk=1 << 17):
             with torch.cuda.stream(st):
                 b["u"][:m * np3].copy_(hu[e0 * np3:e1 * np3],
                                        non_blocking=True)
-                b["g"][:6 * m * np3].copy_(hg[6 * e0 * np3:6 * e1 * np3],
-                                           non_blocking=True)
-                b["d"].copy_(hd, non_blocking=True)
+                if resident:
+                    gd = resident["g"][6 * e0 * np3:6 * e1 * np3]
+                    dd = resident["d"]
+                else:
+                    b["g"][:6 * m * np3].copy_(hg[6 * e0 * np3:6 * e1 * np3],
+                                               non_blocking=True)
+                    b["d"].copy_(hd, non_blocking=True)
+                    gd, dd = b["g"], b["d"]
                 env = lfb.env_from_buffers(
-                    knl, {"nelt": m}, {"u": b["u"], "g": b["g"],
-                                       "w": b["w"], "d": b["d"]})
+                    knl, {"nelt": m}, {"u": b["u"], "g": gd,
+                                       "w": b["w"], "d": dd})
                 lfb.interpret(knl, env, inplace=True)
                 launches[0] += 1
                 hw[e0 * np3:e1 * np3].copy_(b["w"][:m * np3],
@@ -364,15 +371,41 @@ def sem_e2e(knl, n, nelt, dev, steps, chunk=1 << 17):
     e1.record(cur)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / steps
-    return {"value": nelt * np3 / (ms * 1e-3) / 1e9, "unit": "GDOF/s",
-            "h2d_bytes_per_step": (hu.numel() + hg.numel()) * 8
-            + len(chunks) * hd.numel() * 8,
-            "d2h_bytes_per_step": hw.numel() * 8,
-            "ms_per_step": ms, "steps": steps,
+    out = {"value": nelt * np3 / (ms * 1e-3) / 1e9, "unit": "GDOF/s",
+           "h2d_bytes_per_step": (hu.numel() + hg.numel()) * 8
+           + len(chunks) * hd.numel() * 8,
+           "d2h_bytes_per_step": hw.numel() * 8,
+           "ms_per_step": ms, "steps": steps,
+           "gpu_launches": launches[0],
+           "api": "paper_1503_07659_b200.interpret -> lfb_semlap_f64 "
+                  f"(ctypes C-ABI), {len(chunks)} chunks of {chunk} "
+                  "elements on 2 streams; every input (u, g, d) copied "
+                  "host->device every step"}
+    # the operator-application pattern of an iterative solver: geometry
+    # (g, d) set up once on the device (make_device_env-style), each step
+    # moves only the field u in and the result w out
+    try:
+        resident["g"] = hg.to(dev, non_blocking=False)
+        resident["d"] = hd.to(dev)
+        run(1)
+        torch.cuda.synchronize()
+        launches[0] = 0
+        e0.record(cur)
+        run(steps)
+        e1.record(cur)
+        torch.cuda.synchronize()
+        ms2 = e0.elapsed_time(e1) / steps
+        out["resident_geometry"] = {
+            "value": nelt * np3 / (ms2 * 1e-3) / 1e9, "unit": "GDOF/s",
+            "h2d_bytes_per_step": hu.numel() * 8,
+            "d2h_bytes_per_step": hw.numel() * 8, "ms_per_step": ms2,
             "gpu_launches": launches[0],
-            "api": "paper_1503_07659_b200.interpret -> lfb_semlap_f64 "
-                   f"(ctypes C-ABI), {len(chunks)} chunks of {chunk} "
-                   "elements on 2 streams"}
+            "note": "g and d device-resident (uploaded once, outside the "
+                    "timed region); u H2D and w D2H every step"}
+        resident.clear()
+    except RuntimeError as exc:  # device memory
+        out["resident_geometry"] = {"unavailable": str(exc)[:120]}
+    return out
 
 
 def cpu_reference(n, sample_elems, threads, min_seconds):
@@ -696,6 +729,11 @@ def main():
         ms = max_over_ranks(e2e["ms_per_step"], world)
         e2e["value"] = nelt_e2e * world * args.npts ** 3 / (ms * 1e-3) / 1e9
         e2e["ms_per_step"] = ms
+        rg = e2e.get("resident_geometry", {})
+        if "ms_per_step" in rg:
+            ms2 = max_over_ranks(rg["ms_per_step"], world)
+            rg["value"] = nelt_e2e * world * args.npts ** 3 / (ms2 * 1e-3) / 1e9
+            rg["ms_per_step"] = ms2
         res["e2e"] = e2e
     res["cpu_baseline"] = None
     if rank == 0 and world == 1 and not args.no_cpu:

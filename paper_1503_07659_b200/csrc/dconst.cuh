@@ -1,0 +1,87 @@
+// d (the SEM derivative matrix) in the constant bank.
+//
+// Every lane of a warp reads the same d(k,l) in the ut contraction of phase 1
+// and d(l,k) in phase 2.  From shared memory each of those broadcasts costs a
+// full warp-wide LDS (>= 2 L1 wavefronts for one or two doubles), and the SEM
+// kernels are bound by the L1 LSU data pipe (profiles/r01_sem65k.md: 95 %).
+// Held in a __constant__ array indexed with compile-time offsets (the loops
+// are fully unrolled over k and l), d(k,l) becomes an immediate c[bank][off]
+// operand of the DMUL: no load instruction at all.
+//
+// The constant array is per translation unit; a launch first copies d into a
+// slot of it with a stream-ordered device-to-device cudaMemcpyToSymbolAsync.
+// A slot may still be read by a kernel running on another stream, so each
+// slot carries an event: the copy waits for the last kernel that used the
+// slot, and the launch records the event again (dconst_acquire/release).
+// Inside a CUDA graph capture only the copy is recorded (graph order keeps
+// copy and kernel together).
+#pragma once
+
+#include <mutex>
+
+#include "lfb_common.cuh"
+
+namespace lfb {
+
+struct DConstRing {
+  std::mutex mu;
+  cudaEvent_t ev[64] = {};
+  bool used[64] = {};
+  int next = 0;  // for callers that rotate over several slots
+};
+
+inline DConstRing &dconst_ring(int tag, int dev) {
+  static DConstRing rings[4][16];
+  return rings[tag & 3][dev & 15];
+}
+
+// Copies d (n*n doubles, device memory) to `symbol` at byte offset
+// slot * slot_bytes on stream s, ordered after the last launch that read
+// that slot of ring `tag`.  *slot >= 0 names the slot; *slot = -k picks the
+// next of k rotating slots and returns it.  Returns with the ring locked in
+// *lk; the caller launches on s and then calls dconst_release.
+template <typename T>
+inline int dconst_acquire(const T &symbol, size_t slot_bytes, int tag,
+                          int *slot_io, const double *d, int n,
+                          cudaStream_t s, std::unique_lock<std::mutex> *lk,
+                          bool *capturing) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess)
+    return fail(LFB_ERR_LAUNCH, "semlap: cudaGetDevice failed");
+  DConstRing &r = dconst_ring(tag, dev);
+  *lk = std::unique_lock<std::mutex>(r.mu);
+  if (*slot_io < 0) {
+    const int k = -*slot_io;
+    *slot_io = r.next;
+    r.next = (r.next + 1) % k;
+  }
+  const int slot = *slot_io;
+  const size_t off = (size_t)slot * slot_bytes;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(s, &cap);
+  *capturing = cap != cudaStreamCaptureStatusNone;
+  if (!*capturing) {
+    if (!r.ev[slot] && cudaEventCreateWithFlags(&r.ev[slot],
+                                                cudaEventDisableTiming) !=
+                           cudaSuccess)
+      return fail(LFB_ERR_LAUNCH, "semlap: event create failed");
+    if (r.used[slot]) cudaStreamWaitEvent(s, r.ev[slot], 0);
+  }
+  if (cudaMemcpyToSymbolAsync(symbol, d, (size_t)n * n * 8, off,
+                              cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+    return fail(LFB_ERR_LAUNCH,
+                "semlap: copy of d to the constant bank failed");
+  return LFB_OK;
+}
+
+inline void dconst_release(int tag, int slot, cudaStream_t s,
+                           bool capturing) {
+  if (capturing) return;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  DConstRing &r = dconst_ring(tag, dev);  // caller still holds r.mu
+  cudaEventRecord(r.ev[slot], s);
+  r.used[slot] = true;
+}
+
+}  // namespace lfb

@@ -607,7 +607,7 @@ static int sem_dispatch(double *w, const double *u, const double *d,
                                    grid_out);
     if (rc != -1) return rc;
   }
-  const int var = (n == 8 && var0 == 0) ? 39 : var0;  // smem-d n = 8 kernel
+  const int var = var0;
   LFB_SEM_TABLE(S, A)
 #undef S
 #undef A

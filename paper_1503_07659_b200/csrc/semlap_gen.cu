@@ -22,13 +22,18 @@
 //    concurrently streamed chunks are adjacent in HBM.
 //  * Both phases fully unrolled over k and l: n independent accumulation
 //    chains per thread give the FP64 pipe the ILP it needs at low occupancy.
-//  * d in smem in both orientations (dn = d, dt = d^T) so every warp access
-//    is a broadcast or consecutive; optionally the per-thread d rows live in
-//    registers (DREG).
+//  * the broadcast d(k,l) / d(l,k) of the ut contractions come from the
+//    constant bank (dconst.cuh: immediate operands, no LSU traffic); the
+//    per-thread rows d(i,.), d(j,.) from smem (dn = d, dt = d^T), optionally
+//    kept in registers (DREG).
+#include "dconst.cuh"
 #include "lfb_common.cuh"
 #include "semlap_common.cuh"
 
 namespace lfb {
+
+// d(a,b) at c_dgen[N][a + N b] for the order being launched (dconst.cuh)
+__constant__ double c_dgen[12][128];
 
 template <int N, int E>
 struct GenCfg {
@@ -173,13 +178,13 @@ __global__ void __launch_bounds__(G *GenCfg<N, E>::T, 1)
       for (int k = 0; k < N; ++k) {
         const double *row = su + N * j + N2 * k;  // u(., j, k)
         const double *col = su + i + N2 * k;      // u(i, ., k)
-        const double *dk = dt + N * k;            // d(k, .)
         double ur = 0.0, us = 0.0, ut = 0.0;
 #pragma unroll
         for (int l = 0; l + 1 < N; l += 2) {
-          double r0, r1, k0, k1;
+          double r0, r1;
           ld_pair<N>(row + l, r0, r1);
-          ld_pair<N>(dk + l, k0, k1);
+          const double k0 = c_dgen[N][k + N * l];  // d(k,l): constant bank
+          const double k1 = c_dgen[N][k + N * (l + 1)];
           const double a0 = DREG ? da[l] : dn[i + N * l];
           const double a1 = DREG ? da[l + 1] : dn[i + N * (l + 1)];
           const double b0 = DREG ? db[l] : dn[j + N * l];
@@ -197,7 +202,7 @@ __global__ void __launch_bounds__(G *GenCfg<N, E>::T, 1)
           const double b0 = DREG ? db[l] : dn[j + N * l];
           ur = dadd(ur, dmul(a0, row[l]));
           us = dadd(us, dmul(b0, col[N * l]));
-          ut = dadd(ut, dmul(dk[l], ucol[l]));
+          ut = dadd(ut, dmul(c_dgen[N][k + N * l], ucol[l]));
         }
         const double *gp = sge + 6 * (i + N * j + N2 * k);
         const double2 g01 = *reinterpret_cast<const double2 *>(gp);
@@ -228,13 +233,13 @@ __global__ void __launch_bounds__(G *GenCfg<N, E>::T, 1)
       for (int k = 0; k < N; ++k) {
         const double *rr = scr_r + R * j + R * N * k;  // wr(., j, k)
         const double *rs = scr_s + i + R * N * k;      // ws(i, ., k)
-        const double *dk = dn + N * k;                 // d(., k)
         double s = 0.0;
 #pragma unroll
         for (int l = 0; l + 1 < N; l += 2) {
-          double r0, r1, k0, k1;
+          double r0, r1;
           ld_pair<N>(rr + l, r0, r1);
-          ld_pair<N>(dk + l, k0, k1);
+          const double k0 = c_dgen[N][l + N * k];  // d(l,k)
+          const double k1 = c_dgen[N][l + 1 + N * k];
           const double a0 = DREG ? da[l] : dt[i + N * l];
           const double a1 = DREG ? da[l + 1] : dt[i + N * (l + 1)];
           const double b0 = DREG ? db[l] : dt[j + N * l];
@@ -249,7 +254,7 @@ __global__ void __launch_bounds__(G *GenCfg<N, E>::T, 1)
           const double a0 = DREG ? da[l] : dt[i + N * l];
           const double b0 = DREG ? db[l] : dt[j + N * l];
           s = dadd(dadd(dadd(s, dmul(a0, rr[l])), dmul(b0, rs[R * l])),
-                   dmul(dk[l], wt[l]));
+                   dmul(c_dgen[N][l + N * k], wt[l]));
         }
         we[N2 * k] = s;
         if constexpr (SUMSQ) acc = dadd(acc, dmul(s, s));
@@ -287,8 +292,17 @@ static int launch_gen(double *w, const double *u, const double *d,
                  : semlap_gen_kernel<N, E, G, S, DREG, false>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)L::total);
-  k<<<grid, block, L::total, s>>>(w, u, d, g, nelt,
-                                  sumsq ? geom->workspace : nullptr);
+  {
+    std::unique_lock<std::mutex> lk;
+    bool capturing = false;
+    int slot = N;  // one constant slot per order
+    if (int rc = dconst_acquire(c_dgen, 128 * 8, 1, &slot, d, N, s, &lk,
+                                &capturing))
+      return rc;
+    k<<<grid, block, L::total, s>>>(w, u, d, g, nelt,
+                                    sumsq ? geom->workspace : nullptr);
+    dconst_release(1, slot, s, capturing);
+  }
   if (int rc = check_launch("lfb_semlap_f64")) return rc;
   return sumsq ? sem_sumsq_finish(geom->workspace, grid, geom->sumsq, s)
                : LFB_OK;
@@ -325,8 +339,8 @@ static int launch_gen(double *w, const double *u, const double *d,
   X(10, 0, 1, 3, 1, false)      \
   X(10, 20, 1, 2, 1, true)      \
   X(10, 21, 1, 3, 1, true)      \
-  X(11, 0, 1, 2, 1, true)       \
-  X(11, 20, 1, 2, 1, false)
+  X(11, 0, 1, 2, 1, false)       \
+  X(11, 20, 1, 2, 1, true)
 
 int sem_gen_dispatch(int n, int variant, double *w, const double *u,
                      const double *d, const double *g, int64_t nelt,

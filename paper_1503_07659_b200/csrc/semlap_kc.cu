@@ -15,8 +15,8 @@
 //    compile-time offsets, so d(k,l) is an immediate c[bank][offset] operand
 //    of the DMUL -- no load instruction at all.  The slot is filled by a
 //    stream-ordered device-to-device copy before the launch; a ring of
-//    SLOTS slots with one event each keeps launches on other streams from
-//    overwriting a slot a running kernel still reads (kc_acquire).
+//    KC_SLOTS slots with one event each keeps launches on other streams
+//    from overwriting a slot a running kernel still reads (dconst.cuh).
 //  * the per-thread d rows d(i,.), d(j,.) (phase 1) and d(.,i), d(.,j)
 //    (phase 2) are registers, loaded per phase from the constant slot;
 //  * u is transposed once per element into uT so the u(i,.,k) columns are
@@ -27,8 +27,7 @@
 // Everything else follows semlap_kernel: persistent CTAs of G groups of n^2
 // threads, thread (i,j) owns the k-column (i,j,*), u + g of a whole element
 // by bulk copies (TMA engine) into an SG-deep per-group ring.
-#include <mutex>
-
+#include "dconst.cuh"
 #include "lfb_common.cuh"
 #include "semlap_common.cuh"
 
@@ -215,54 +214,6 @@ __global__ void __launch_bounds__(G *KcCfg<N>::T, 1)
   if constexpr (SUMSQ) block_sumsq_partial(acc, partials);
 }
 
-// {{{ constant-slot ring
-
-struct KcRing {
-  std::mutex mu;
-  int next = 0;
-  cudaEvent_t ev[KC_SLOTS] = {};
-  bool used[KC_SLOTS] = {};
-};
-
-static KcRing &kc_ring(int dev) {
-  static KcRing rings[64];
-  return rings[dev & 63];
-}
-
-// Copy d (n*n doubles, device memory) into a free constant slot on `s`,
-// ordered after the last kernel that read that slot (on any stream).  The
-// caller launches on `s` and then calls kc_release.
-static int kc_acquire(const double *d, int n, cudaStream_t s, int *slot,
-                      std::unique_lock<std::mutex> *lk) {
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess)
-    return fail(LFB_ERR_LAUNCH, "semlap: cudaGetDevice failed");
-  KcRing &r = kc_ring(dev);
-  *lk = std::unique_lock<std::mutex>(r.mu);
-  const int k = r.next;
-  r.next = (r.next + 1) % KC_SLOTS;
-  if (!r.ev[k] &&
-      cudaEventCreateWithFlags(&r.ev[k], cudaEventDisableTiming) != cudaSuccess)
-    return fail(LFB_ERR_LAUNCH, "semlap: event create failed");
-  if (r.used[k]) cudaStreamWaitEvent(s, r.ev[k], 0);
-  if (cudaMemcpyToSymbolAsync(c_dmat, d, (size_t)n * n * 8,
-                              (size_t)k * KC_MAXN2 * 8,
-                              cudaMemcpyDeviceToDevice, s) != cudaSuccess)
-    return fail(LFB_ERR_LAUNCH, "semlap: copy of d to the constant bank failed");
-  *slot = k;
-  return LFB_OK;
-}
-
-static void kc_release(int slot, cudaStream_t s) {
-  int dev = 0;
-  cudaGetDevice(&dev);
-  KcRing &r = kc_ring(dev);  // caller still holds r.mu
-  cudaEventRecord(r.ev[slot], s);
-  r.used[slot] = true;
-}
-
-// }}}
-
 template <int N, int G, int SG, int SLOT>
 static void kc_launch_slot(bool sumsq, int grid, size_t smem, double *w,
                            const double *u, const double *g, int64_t nelt,
@@ -295,16 +246,19 @@ static int launch_kc(double *w, const double *u, const double *d,
   if (sumsq && (!geom->workspace || geom->workspace_len < grid))
     return fail(LFB_ERR_ARG, "semlap: sumsq workspace too small");
   double *part = sumsq ? geom->workspace : nullptr;
-  int slot = 0;
   std::unique_lock<std::mutex> lk;
-  if (int rc = kc_acquire(d, N, s, &slot, &lk)) return rc;
+  bool capturing = false;
+  int slot = -KC_SLOTS;  // rotate over the slots
+  if (int rc = dconst_acquire(c_dmat, KC_MAXN2 * 8, 0, &slot, d, N, s, &lk,
+                              &capturing))
+    return rc;
   switch (slot) {
     case 0: kc_launch_slot<N, G, SG, 0>(sumsq, grid, L::total, w, u, g, nelt, part, s); break;
     case 1: kc_launch_slot<N, G, SG, 1>(sumsq, grid, L::total, w, u, g, nelt, part, s); break;
     case 2: kc_launch_slot<N, G, SG, 2>(sumsq, grid, L::total, w, u, g, nelt, part, s); break;
     default: kc_launch_slot<N, G, SG, 3>(sumsq, grid, L::total, w, u, g, nelt, part, s); break;
   }
-  kc_release(slot, s);
+  dconst_release(0, slot, s, capturing);
   lk.unlock();
   if (int rc = check_launch("lfb_semlap_f64")) return rc;
   return sumsq ? sem_sumsq_finish(geom->workspace, grid, geom->sumsq, s)
@@ -322,12 +276,7 @@ int sem_kc_dispatch(int n, int variant, double *w, const double *u,
                     const double *d, const double *g, int64_t nelt,
                     const lfb_launch *geom, cudaStream_t s,
                     int64_t *grid_out) {
-  // the slot ring orders launches with events; inside a CUDA graph capture
-  // the caller gets the shared-memory-d kernel instead
-  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-  if (!grid_out && cudaStreamIsCapturing(s, &cap) == cudaSuccess &&
-      cap != cudaStreamCaptureStatusNone)
-    return -1;
+
 #define X(NN, VV, GG, SS)                                                   \
   if (n == NN && variant == VV)                                             \
     return launch_kc<NN, GG, SS>(w, u, d, g, nelt, geom, s, grid_out);

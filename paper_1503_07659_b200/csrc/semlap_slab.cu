@@ -16,19 +16,36 @@
 //  * g: the phase-1 combine at slab k needs only g(:, :, :, k) = 6 n^2
 //    doubles (48 n^2 bytes, always 16-byte aligned), streamed through an
 //    SGS-deep slab ring, one bulk copy per slab, issued SGS slabs ahead.
-//  * wr/ws: padded smem scratch (row stride n+1), wt and the u column in
-//    registers, d from smem.
+//  * wr/ws: padded smem scratch (row stride n+2 for even n so wr rows load
+//    as 16-byte pairs, n+1 for odd n), wt and the u column in registers;
+//    the broadcast d(k,l) / d(l,k) are constant-bank operands (dconst.cuh),
+//    the per-thread d rows come from smem or registers (DREG).
+#include "dconst.cuh"
 #include "lfb_common.cuh"
 #include "semlap_common.cuh"
 
 namespace lfb {
+
+// d(a,b) at c_dslab[N][a + N b] for the order being launched (dconst.cuh)
+__constant__ double c_dslab[17][256];
+
+template <int N>
+__device__ __forceinline__ void slab_pair(const double *p, double &a,
+                                          double &b) {
+  if constexpr (N % 2 == 0) {
+    const double2 v = *reinterpret_cast<const double2 *>(p);
+    a = v.x, b = v.y;
+  } else {
+    a = p[0], b = p[1];
+  }
+}
 
 template <int N>
 struct SlabCfg {
   static constexpr int N2 = N * N;
   static constexpr int NP = N * N * N;
   static constexpr int T = ((N2 + 31) / 32) * 32;
-  static constexpr int R = N + 1;
+  static constexpr int R = (N % 2 == 0) ? N + 2 : N + 1;  // even: pairs
   static constexpr int SCR = R * N * N;
   static constexpr int UST = (NP + 2 + 1) / 2 * 2;  // + 8-byte lead, even
   static constexpr int SLAB = 6 * N2;
@@ -179,14 +196,21 @@ __global__ void __launch_bounds__(G *SlabCfg<N>::T, 1)
             double ur = 0.0, us = 0.0, ut = 0.0;
             const double *row = su + N * j + N2 * k;
             const double *col = su + i + N2 * k;
-            const double *dk = dt + N * k;  // d(k, .)
 #pragma unroll
-            for (int l = 0; l < N; ++l) {
-              const double a = DREG ? da[l] : dn[i + N * l];
-              const double b = DREG ? db[l] : dn[j + N * l];
-              ur = dadd(ur, dmul(a, row[l]));
-              us = dadd(us, dmul(b, col[N * l]));
-              ut = dadd(ut, dmul(dk[l], ucol[l]));
+            for (int l = 0; l < N; l += 2) {
+              double r0, r1 = 0.0;
+              if (l + 1 < N) slab_pair<N>(row + l, r0, r1);
+              else r0 = row[l];
+#pragma unroll
+              for (int h = 0; h < 2 && l + h < N; ++h) {
+                const int ll = l + h;
+                const double a = DREG ? da[ll] : dn[i + N * ll];
+                const double b = DREG ? db[ll] : dn[j + N * ll];
+                ur = dadd(ur, dmul(a, h ? r1 : r0));
+                us = dadd(us, dmul(b, col[N * ll]));
+                // d(k,l): an immediate constant-bank operand
+                ut = dadd(ut, dmul(c_dslab[N][k + N * ll], ucol[ll]));
+              }
             }
             const double *gp = gs + kk * C::SLAB + 6 * (i + N * j);
             const double2 g01 = *reinterpret_cast<const double2 *>(gp);
@@ -225,13 +249,20 @@ __global__ void __launch_bounds__(G *SlabCfg<N>::T, 1)
         double s = 0.0;
         const double *rr = scr_r + R * j + R * N * k;  // wr(., j, k)
         const double *rs = scr_s + i + R * N * k;      // ws(i, ., k)
-        const double *dk = dn + N * k;                 // d(., k)
 #pragma unroll
-        for (int l = 0; l < N; ++l) {
-          const double a = DREG ? da[l] : dt[i + N * l];
-          const double b = DREG ? db[l] : dt[j + N * l];
-          s = dadd(dadd(dadd(s, dmul(a, rr[l])), dmul(b, rs[R * l])),
-                   dmul(dk[l], wt[l]));
+        for (int l = 0; l < N; l += 2) {
+          double r0, r1 = 0.0;
+          if (l + 1 < N) slab_pair<N>(rr + l, r0, r1);
+          else r0 = rr[l];
+#pragma unroll
+          for (int h = 0; h < 2 && l + h < N; ++h) {
+            const int ll = l + h;
+            const double a = DREG ? da[ll] : dt[i + N * ll];
+            const double b = DREG ? db[ll] : dt[j + N * ll];
+            s = dadd(dadd(dadd(s, dmul(a, h ? r1 : r0)),
+                          dmul(b, rs[R * ll])),
+                     dmul(c_dslab[N][ll + N * k], wt[ll]));  // d(l,k)
+          }
         }
         we[N2 * k] = s;
         if constexpr (SUMSQ) acc = dadd(acc, dmul(s, s));
@@ -268,8 +299,17 @@ int launch_sem_slab(double *w, const double *u, const double *d,
                  : semlap_slab_kernel<N, G, SGS, KS, DREG, false>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)L::total);
-  k<<<grid, block, L::total, s>>>(w, u, d, g, nelt,
-                                  sumsq ? geom->workspace : nullptr);
+  {
+    std::unique_lock<std::mutex> lk;
+    bool capturing = false;
+    int slot = N;  // one constant slot per order
+    if (int rc = dconst_acquire(c_dslab, 256 * 8, 2, &slot, d, N, s, &lk,
+                                &capturing))
+      return rc;
+    k<<<grid, block, L::total, s>>>(w, u, d, g, nelt,
+                                    sumsq ? geom->workspace : nullptr);
+    dconst_release(2, slot, s, capturing);
+  }
   if (int rc = check_launch("lfb_semlap_f64")) return rc;
   return sumsq ? sem_sumsq_finish(geom->workspace, grid, geom->sumsq, s)
                : LFB_OK;
@@ -288,19 +328,19 @@ int launch_sem_slab(double *w, const double *u, const double *d,
   X(9, 0, 4, 4, 1, false)       \
   X(10, 0, 4, 4, 1, false)      \
   X(11, 0, 3, 4, 1, false)      \
-  X(12, 0, 2, 4, 2, true)       \
+  X(12, 0, 2, 3, 2, true)       \
   X(12, 30, 2, 4, 1, false)     \
   X(12, 31, 3, 2, 1, false)     \
-  X(13, 0, 2, 4, 1, false)      \
-  X(13, 31, 2, 4, 1, true)      \
+  X(13, 0, 2, 4, 1, true)       \
+  X(13, 31, 2, 4, 1, false)      \
   X(14, 0, 1, 4, 2, true)       \
   X(14, 30, 1, 4, 1, false)     \
   X(14, 31, 1, 3, 2, false)     \
   X(15, 0, 1, 3, 2, false)      \
   X(15, 30, 1, 4, 1, false)     \
-  X(16, 0, 1, 3, 2, false)      \
+  X(16, 0, 1, 2, 3, false)      \
   X(16, 30, 1, 3, 1, false)     \
-  X(16, 31, 1, 2, 3, false)
+  X(16, 31, 1, 3, 2, false)
 
 int sem_slab_dispatch(int n, int variant, double *w, const double *u,
                       const double *d, const double *g, int64_t nelt,
