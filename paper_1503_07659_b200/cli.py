@@ -3,7 +3,10 @@ unimplemented CLI (pyproject.toml:15-16 names ``loopforge.cli:main``; the
 command set is SPEC.md:703-742), with ``run`` executing on the B200.
 
     python -m paper_1503_07659_b200 run <file.f> --param n=32 \\
-        --in u=u.bin [--scalar alpha=1.5] --out result=r.bin
+        --in u=u.bin [--scalar alpha=1.5] --out result=r.bin [--flat-out]
+
+An input file holds either the logical array or, 1-D, the flat strided
+buffer (interp.py FlatArray.data / the emitted C's arrays).
     python -m paper_1503_07659_b200 translate <file.f> --target c|opencl|cuda
     python -m paper_1503_07659_b200 dump-ir <file.f> --stage raw|transformed|expanded
     python -m paper_1503_07659_b200 check <file.f> [--param n=32]
@@ -112,7 +115,8 @@ def cmd_run(args):
     import torch
 
     from . import arrayio
-    from .executor import get_device_output, interpret, make_device_env
+    from .executor import (_flat_size, get_device_output, interpret,
+                           make_device_env)
     _raw, knl = _translate(args)
     params = _kv(args.param, "--param", int)
     missing = [p for p in knl.param_names if p not in params]
@@ -125,27 +129,38 @@ def cmd_run(args):
         raise InterpError("run mode executes on the B200: no CUDA device "
                           "(there is no CPU fallback)")
     dev = torch.device("cuda", args.device)
-    inputs = {}
-    dtypes = {a.name: a.dtype for a in knl.args}
+    inputs, flat = {}, {}
+    argmap = {a.name: a for a in knl.args}
     for name, path in _kv(args.inputs, "--in", str).items():
-        if name not in dtypes:
+        if name not in argmap:
             from ._loopforge import InterpError
             raise InterpError(f"--in {name}: the kernel has no argument "
                               f"'{name}'")
-        t = arrayio.read_array_file(path, dev, dtypes[name])
-        scalar = next(a for a in knl.args if a.name == name).kind \
-            == "scalar-value"
-        inputs[name] = t.item() if scalar else t
+        a = argmap[name]
+        t = arrayio.read_array_file(path, dev, a.dtype)
+        if a.kind == "scalar-value":
+            inputs[name] = t.item()
+            continue
+        shape = tuple(s.eval(params) for s in a.shape)
+        strides = tuple(s.eval(params) for s in a.strides)
+        if t.dim() == 1 and tuple(t.shape) != shape and \
+                t.numel() == _flat_size(shape, strides):
+            flat[name] = t  # the flat strided buffer itself (FlatArray.data)
+        else:
+            inputs[name] = t  # logical shape
     for name, v in _kv(args.scalar, "--scalar", float).items():
         inputs[name] = v
     env = make_device_env(knl, params, inputs, seed=args.seed, device=dev)
+    for name, t in flat.items():
+        env.arrays[name].data.copy_(t)
     t0 = time.perf_counter()
     out = interpret(knl, env, variant=args.variant, engine=args.engine)
     torch.cuda.synchronize(dev)
     t1 = time.perf_counter()
     outs = _kv(args.outputs, "--out", str)
     for name, path in outs.items():
-        arrayio.write_array_file(path, get_device_output(out, name))
+        arrayio.write_array_file(path, out.arrays[name].data if args.flat_out
+                                 else get_device_output(out, name))
     if args.verbose:
         print(json.dumps({"kernel": knl.name, "params": params,
                           "outputs": sorted(outs), "seconds": t1 - t0}),
@@ -193,6 +208,9 @@ def main(argv=None):
     p.add_argument("--in", dest="inputs", action="append")
     p.add_argument("--scalar", action="append")
     p.add_argument("--out", dest="outputs", action="append")
+    p.add_argument("--flat-out", action="store_true",
+                   help="write the flat strided buffers (the emitted C's "
+                        "arrays) instead of logical-shape arrays")
     p.add_argument("--seed", type=int, default=None,
                    help="fill unspecified inputs like make_env(seed=...)")
     p.add_argument("--engine", choices=["auto", "kernels", "generic"],

@@ -142,6 +142,7 @@ def test_cli_run_matches_reference_goldens(cuda, name, tmp_path):
     outs = g.outputs()
     for a in outs:
         argv += ["--out", f"{a}={tmp_path}/{a}.bin"]
+    argv.append("--flat-out")  # the goldens hold the flat buffers
     assert main(argv) == 0
     for a in outs:
         got = read_array_file(f"{tmp_path}/{a}.bin")
