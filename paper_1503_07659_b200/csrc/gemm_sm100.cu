@@ -310,6 +310,33 @@ constexpr int TC2_EPI_WARPS = 16;
 constexpr int TC2_THREADS = 32 * (2 + TC2_EPI_WARPS);  // producer, MMA, epi
 constexpr int TC2_GROUP_M = 8;  // M tiles per raster group
 
+// BK = 32: 128-byte swizzled K rows, 2 stages of 96 KB; BK = 16: 64-byte
+// swizzled rows, 4 stages of 48 KB -- the same bytes in flight, but a stage
+// is refilled after 6 instead of 12 MMAs, which gives the TMA loads three
+// stages of slack instead of one.
+template <int BK>
+struct Tc2Cfg {
+  static constexpr int STAGES = BK == 32 ? 2 : 4;
+  static constexpr int CHUNK = 256 / BK;  // k-slabs per TMEM chunk (K = 256)
+  static constexpr size_t a_bytes = (size_t)TC_BM * BK * 4;
+  static constexpr size_t b_bytes = (size_t)TC_BN * BK * 4;
+  static constexpr size_t stage_bytes = 2 * a_bytes + 2 * b_bytes;
+  static constexpr size_t bars_off = STAGES * stage_bytes;
+  static constexpr size_t total = bars_off + 256 + 1024;
+  // K-major smem descriptor: rows of BK*4 bytes, 8-row swizzle atoms
+  // (SBO = 8 rows), layout type 2 = SWIZZLE_128B, 4 = SWIZZLE_64B (sm100)
+  __device__ static uint64_t desc(const void *smem) {
+    const uint64_t addr = smem_u32(smem);
+    uint64_t d = 0;
+    d |= (addr >> 4) & 0x3FFFull;
+    d |= (uint64_t)1 << 16;
+    d |= (uint64_t)((8 * BK * 4) >> 4) << 32;
+    d |= (uint64_t)1 << 46;
+    d |= (uint64_t)(BK == 32 ? 2 : 4) << 61;
+    return d;
+  }
+};
+
 __device__ __forceinline__ void tc2_tile(int t, int mt_count, int nt_count,
                                          int *mt, int *nt) {
   const int per_group = TC2_GROUP_M * nt_count;
@@ -321,29 +348,31 @@ __device__ __forceinline__ void tc2_tile(int t, int mt_count, int nt_count,
   *nt = r / gm;
 }
 
+template <int BK>
 __global__ void __launch_bounds__(TC2_THREADS, 1)
     sgemm_tc2_kernel(const __grid_constant__ CUtensorMap map_ahi,
                      const __grid_constant__ CUtensorMap map_alo,
                      const __grid_constant__ CUtensorMap map_bhi,
                      const __grid_constant__ CUtensorMap map_blo, float alpha,
                      float *__restrict__ c, int l, int m, int n) {
+  using C = Tc2Cfg<BK>;
   extern __shared__ unsigned char smem_raw[];
   unsigned char *smem = reinterpret_cast<unsigned char *>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t *full = reinterpret_cast<uint64_t *>(smem + TcSmem::bars_off);
-  uint64_t *empty = full + TC_STAGES;
-  uint64_t *acc_full = empty + TC_STAGES;  // [2] MMA -> epilogue
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + C::bars_off);
+  uint64_t *empty = full + C::STAGES;
+  uint64_t *acc_full = empty + C::STAGES;  // [2] MMA -> epilogue
   uint64_t *acc_empty = acc_full + 2;      // [2] epilogue -> MMA
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(acc_empty + 2);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int nk = l / TC_BK;
-  const int nchunks = (nk + TC_CHUNK - 1) / TC_CHUNK;
+  const int nk = l / BK;
+  const int nchunks = (nk + C::CHUNK - 1) / C::CHUNK;
   const int mt_count = m / TC_BM, nt_count = n / TC_BN;
   const int ntiles = mt_count * nt_count;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < TC_STAGES; ++s) {
+    for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
@@ -366,7 +395,7 @@ __global__ void __launch_bounds__(TC2_THREADS, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  auto stage_ptr = [&](int s) { return smem + s * TcSmem::stage_bytes; };
+  auto stage_ptr = [&](int s) { return smem + s * C::stage_bytes; };
 
   if (warp == 0) {
     if (lane == 0) {
@@ -376,15 +405,15 @@ __global__ void __launch_bounds__(TC2_THREADS, 1)
         tc2_tile(t, mt_count, nt_count, &mt, &nt);
         const int i0 = mt * TC_BM, j0 = nt * TC_BN;
         for (int kb = 0; kb < nk; ++kb, ++it) {
-          const int s = it % TC_STAGES;
-          mbar_wait(&empty[s], ((it / TC_STAGES) & 1) ^ 1);
+          const int s = it % C::STAGES;
+          mbar_wait(&empty[s], ((it / C::STAGES) & 1) ^ 1);
           unsigned char *st = stage_ptr(s);
-          mbar_arrive_expect_tx(&full[s], (uint32_t)TcSmem::stage_bytes);
-          const int k0 = kb * TC_BK;
+          mbar_arrive_expect_tx(&full[s], (uint32_t)C::stage_bytes);
+          const int k0 = kb * BK;
           tma_load_2d(st, &map_ahi, k0, i0, &full[s]);
-          tma_load_2d(st + TcSmem::a_bytes, &map_alo, k0, i0, &full[s]);
-          tma_load_2d(st + 2 * TcSmem::a_bytes, &map_bhi, k0, j0, &full[s]);
-          tma_load_2d(st + 2 * TcSmem::a_bytes + TcSmem::b_bytes, &map_blo,
+          tma_load_2d(st + C::a_bytes, &map_alo, k0, i0, &full[s]);
+          tma_load_2d(st + 2 * C::a_bytes, &map_bhi, k0, j0, &full[s]);
+          tma_load_2d(st + 2 * C::a_bytes + C::b_bytes, &map_blo,
                       k0, j0, &full[s]);
         }
       }
@@ -394,25 +423,25 @@ __global__ void __launch_bounds__(TC2_THREADS, 1)
     int it = 0, g = 0;  // k-slab and chunk counters over all tiles
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
       for (int kb = 0; kb < nk; ++kb, ++it) {
-        const int s = it % TC_STAGES;
-        const bool first_in_chunk = (kb % TC_CHUNK) == 0;
+        const int s = it % C::STAGES;
+        const bool first_in_chunk = (kb % C::CHUNK) == 0;
         const bool last_in_chunk =
-            kb % TC_CHUNK == TC_CHUNK - 1 || kb == nk - 1;
+            kb % C::CHUNK == C::CHUNK - 1 || kb == nk - 1;
         const int b = g & 1;
         if (first_in_chunk)  // chunk g - 2 folded out of A(b)
           mbar_wait(&acc_empty[b], ((g >> 1) & 1) ^ 1);
-        mbar_wait(&full[s], (it / TC_STAGES) & 1);
+        mbar_wait(&full[s], (it / C::STAGES) & 1);
         tc_fence_after();
         if (lane == 0) {
           unsigned char *st = stage_ptr(s);
-          const uint64_t ahi = sw128_kmajor_desc(st);
-          const uint64_t alo = sw128_kmajor_desc(st + TcSmem::a_bytes);
-          const uint64_t bhi = sw128_kmajor_desc(st + 2 * TcSmem::a_bytes);
+          const uint64_t ahi = C::desc(st);
+          const uint64_t alo = C::desc(st + C::a_bytes);
+          const uint64_t bhi = C::desc(st + 2 * C::a_bytes);
           const uint64_t blo =
-              sw128_kmajor_desc(st + 2 * TcSmem::a_bytes + TcSmem::b_bytes);
+              C::desc(st + 2 * C::a_bytes + C::b_bytes);
           const uint32_t acc = tmem + (uint32_t)(b * TC_BN);
 #pragma unroll
-          for (int k = 0; k < TC_BK / 8; ++k) {
+          for (int k = 0; k < BK / 8; ++k) {
             const uint64_t dk = (uint64_t)((k * 32) >> 4);
             tc_mma_tf32(acc, alo + dk, bhi + dk, idesc,
                         !(first_in_chunk && k == 0));
@@ -546,16 +575,17 @@ static PFN_cuTensorMapEncodeTiled_v12000 tc_encode_fn() {
 }
 
 static bool make_kmajor_map(CUtensorMap *map, const float *base, int rows,
-                            int kdim, int box_rows) {
+                            int kdim, int box_rows, int bk = TC_BK) {
   auto encode = tc_encode_fn();
   if (!encode) return false;
   cuuint64_t dims[2] = {(cuuint64_t)kdim, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)kdim * 4};
-  cuuint32_t box[2] = {(cuuint32_t)TC_BK, (cuuint32_t)box_rows};
+  cuuint32_t box[2] = {(cuuint32_t)bk, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
   return encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
                 const_cast<float *>(base), dims, strides, box, estr,
-                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                CU_TENSOR_MAP_INTERLEAVE_NONE,
+                bk == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
@@ -570,9 +600,33 @@ bool sgemm_tc_shape_ok(int l, int m, int n) {
 }
 
 // returns < 0 when the shape/workspace does not allow the tensor-core path
+template <int BK>
+static int launch_tc2(const float *ahi, const float *alo, const float *bhi,
+                      const float *blo, float alpha, float *c, int l, int m,
+                      int n, cudaStream_t s) {
+  using C = Tc2Cfg<BK>;
+  CUtensorMap mah, mal, mbh, mbl;
+  if (!make_kmajor_map(&mah, ahi, m, l, TC_BM, BK) ||
+      !make_kmajor_map(&mal, alo, m, l, TC_BM, BK) ||
+      !make_kmajor_map(&mbh, bhi, n, l, TC_BN, BK) ||
+      !make_kmajor_map(&mbl, blo, n, l, TC_BN, BK))
+    return fail(LFB_ERR_LAUNCH, "sgemm: tensor map encode failed");
+  cudaFuncSetAttribute(sgemm_tc2_kernel<BK>,
+                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)C::total);
+  int sms = sm_count(nullptr);
+  if (sms <= 0) sms = 148;
+  const int tiles = (m / TC_BM) * (n / TC_BN);
+  sgemm_tc2_kernel<BK><<<tiles < sms ? tiles : sms, TC2_THREADS, C::total,
+                         s>>>(mah, mal, mbh, mbl, alpha, c, l, m, n);
+  return check_launch("lfb_sgemm_f32(tcgen05 persistent)");
+}
+
+// variant: 0/2 persistent BK=16 (default), 3 the first non-persistent
+// kernel, 4 persistent BK=32
 int sgemm_tc(float alpha, const float *a, const float *b, float *c, int l,
              int m, int n, float *ws, int64_t ws_floats, cudaStream_t s,
-             bool persistent) {
+             int variant) {
   if (!sgemm_tc_shape_ok(l, m, n) || !ws ||
       ws_floats < sgemm_tc_workspace_floats(l, m, n) || !aligned(ws, 16))
     return -1;
@@ -582,33 +636,16 @@ int sgemm_tc(float alpha, const float *a, const float *b, float *c, int l,
       a, ahi, alo, m, l);
   const int64_t nb = (int64_t)l * n;
   split_kernel<<<sm_count(nullptr) * 8, 256, 0, s>>>(b, bhi, blo, nb);
+  if (variant == 4)
+    return launch_tc2<32>(ahi, alo, bhi, blo, alpha, c, l, m, n, s);
+  if (variant != 3)
+    return launch_tc2<16>(ahi, alo, bhi, blo, alpha, c, l, m, n, s);
   CUtensorMap mah, mal, mbh, mbl;
   if (!make_kmajor_map(&mah, ahi, m, l, TC_BM) ||
       !make_kmajor_map(&mal, alo, m, l, TC_BM) ||
       !make_kmajor_map(&mbh, bhi, n, l, TC_BN) ||
       !make_kmajor_map(&mbl, blo, n, l, TC_BN))
     return fail(LFB_ERR_LAUNCH, "sgemm: tensor map encode failed");
-  if (persistent) {
-    cudaFuncSetAttribute(sgemm_tc2_kernel,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)TcSmem::total);
-    int sms = sm_count(nullptr);
-    if (sms <= 0) sms = 148;
-    const int tiles = (m / TC_BM) * (n / TC_BN);
-    sgemm_tc2_kernel<<<tiles < sms ? tiles : sms, TC2_THREADS, TcSmem::total,
-                       s>>>(mah, mal, mbh, mbl, alpha, c, l, m, n);
-    if (cudaPeekAtLastError() != cudaSuccess) {
-      cudaFuncAttributes fa{};
-      cudaFuncGetAttributes(&fa, sgemm_tc2_kernel);
-      cudaGetLastError();
-      return fail(LFB_ERR_LAUNCH,
-                  "lfb_sgemm_f32(tcgen05 persistent): launch failed "
-                  "(regs %d, max threads %d, local %zu, smem %zu)",
-                  fa.numRegs, fa.maxThreadsPerBlock, fa.localSizeBytes,
-                  (size_t)TcSmem::total);
-    }
-    return check_launch("lfb_sgemm_f32(tcgen05)");
-  }
   cudaFuncSetAttribute(sgemm_tc_kernel,
                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)TcSmem::total);

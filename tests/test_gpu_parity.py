@@ -391,7 +391,7 @@ def test_wrong_shape_input_is_interp_error(cuda):
 
 # {{{ sgemm on tensor cores (tolerance parity)
 
-@pytest.mark.parametrize("variant", [2, 3])
+@pytest.mark.parametrize("variant", [2, 3, 4])
 @pytest.mark.parametrize("m,n,l", [(128, 256, 32), (256, 512, 256),
                                    (1024, 768, 4096), (384, 256, 8192),
                                    (3200, 3072, 64), (4096, 2048, 512)])
