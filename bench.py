@@ -215,10 +215,23 @@ def sem_bench(args, rank, world, local):
     u, d, g, w = sem_buffers(n, nelt, dev, 1000 + rank)
     env = lfb.env_from_buffers(knl, {"nelt": nelt},
                                {"u": u, "d": d, "g": g, "w": w})
-    launcher = lfb.Launcher(knl, env, variant=args.variant)
+    sem_variant = args.variant if args.variant is not None else 50
+    launcher = lfb.Launcher(knl, env, variant=sem_variant)
 
     ms, ms_local, clocks = timed(launcher.launch, args.steps, args.warmup,
                                  world, local)
+    # the bitwise kernel (the reference's separately rounded arithmetic)
+    # on the same buffers, same timing method
+    bitwise = None
+    if sem_variant != 0:
+        lb = lfb.Launcher(knl, env, variant=0)
+        ms_b, ms_b_local, clocks_b = timed(lb.launch, args.steps,
+                                           args.warmup, world, local)
+        bitwise = {"variant": 0, "parity": "bitwise",
+                   "value": nelt_total * np3 / (ms_b * 1e-3) / 1e9,
+                   "ms_per_step": ms_b,
+                   "roofline_frac": 64 * np3 * nelt / (ms_b_local * 1e-3)
+                   / 1e9 / _peaks()[0], "clocks": clocks_b}
     value = nelt_total * np3 / (ms * 1e-3) / 1e9
     bytes_per_launch = 64 * np3 * nelt
     achieved = bytes_per_launch / (ms_local * 1e-3) / 1e9
@@ -247,9 +260,11 @@ def sem_bench(args, rank, world, local):
                                                                 None))),
                      dtype=torch.float64, device=dev)
     ss = torch.zeros(1, dtype=torch.float64, device=dev)
-    lfb.Launcher(knl, env, sumsq=ss, workspace=ws).launch()
+    lfb.Launcher(knl, env, sumsq=ss, workspace=ws,
+                 variant=sem_variant).launch()
     torch.cuda.synchronize()
-    verify = {"sumsq_allreduced": allreduce_sum(float(ss.item()))}
+    verify = {"sumsq_allreduced": allreduce_sum(float(ss.item())),
+              "variant": sem_variant}
     if not args.no_verify:
         sys.path.insert(0, os.path.join(REPO, "oracle"))
         import oracle
@@ -257,11 +272,21 @@ def sem_bench(args, rank, world, local):
         for tag, e0 in (("head", 0), ("tail", nelt - ns)):
             uh = u[e0 * np3:(e0 + ns) * np3].cpu().numpy()
             gh = g[6 * e0 * np3:6 * (e0 + ns) * np3].cpu().numpy()
-            ref = oracle.semlap(np.zeros_like(uh), uh, d.cpu().numpy(), gh,
-                                n, ns, threads=8)
+            dh = d.cpu().numpy()
+            ref = oracle.semlap(np.zeros_like(uh), uh, dh, gh, n, ns,
+                                threads=8)
+            got = w[e0 * np3:(e0 + ns) * np3].cpu().numpy()
             verify[f"bitwise_{tag}_{ns}_elements"] = bool(
-                w[e0 * np3:(e0 + ns) * np3].cpu().numpy().tobytes()
-                == ref.tobytes())
+                got.tobytes() == ref.tobytes())
+            if sem_variant == 50:
+                # per point against the magnitude of the summed terms
+                mag = oracle.semlap(np.zeros_like(uh), np.abs(uh),
+                                    np.abs(dh), np.abs(gh), n, ns,
+                                    threads=8)
+                verify[f"max_err_over_magnitude_{tag}"] = float(
+                    (np.abs(got - ref) / mag).max())
+        if sem_variant == 50:
+            verify["tolerance"] = 1e-12
 
     res = {
         "metric": METRIC, "value": value, "unit": "GDOF/s",
@@ -274,25 +299,31 @@ def sem_bench(args, rank, world, local):
                    "nelt": nelt_total, "npts": n, "block": block,
                    "parallelism": f"element shards x{world}",
                    "l2": "no flush: inputs 56 B/dof >> 126 MB L2",
-                   "variant": args.variant},
+                   "variant": sem_variant,
+                   "parity": "bitwise" if sem_variant != 50 else
+                   "fp64 within 1e-12 of the reference (each multiply-add "
+                   "one DFMA, same association; per-point bound vs the "
+                   "oracle in verify and tests)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak,
                      "traffic": _traffic(f"semlap_n{n}"),
                      "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": bytes_per_launch,
-                     "kernel": "semlap_kc_kernel (1 launch per step, after "
-                               "a 512 B d -> constant-bank copy)",
+                     "kernel": f"semlap_kc_kernel variant {sem_variant} "
+                               "(1 launch per step, after a 512 B d -> "
+                               "constant-bank copy)",
                      "stream_probe_gbs": probe_gbs,
                      "stream_probe_note": "same buffers, same bytes, no "
                                           "arithmetic (lfb_probe_stream)"},
         "clocks": clocks, "gpu_launches": args.steps, "verify": verify,
+        "bitwise": bitwise,
     }
     del env, launcher, u, d, g, w, ws
     torch.cuda.empty_cache()
     return res, knl
 
 
-def sem_e2e(knl, n, nelt, dev, steps, chunk=1 << 17):
+def sem_e2e(knl, n, nelt, dev, steps, chunk=1 << 17, variant=0):
     """Same metric through the public API with HOST buffers.  Every step:
     H2D of all kernel inputs (u, g, d) from pinned host memory, interpret(),
     D2H of the output w.  The elements are processed in chunks (each chunk
@@ -346,7 +377,7 @@ def sem_e2e(knl, n, nelt, dev, steps, chunk=1 << 17):
                 env = lfb.env_from_buffers(
                     knl, {"nelt": m}, {"u": b["u"], "g": gd,
                                        "w": b["w"], "d": dd})
-                lfb.interpret(knl, env, inplace=True)
+                lfb.interpret(knl, env, inplace=True, variant=variant)
                 launches[0] += 1
                 hw[e0 * np3:e1 * np3].copy_(b["w"][:m * np3],
                                             non_blocking=True)
@@ -639,17 +670,21 @@ def other_bench(args, local):
             u, d, g, w = sem_buffers(n, nelt, dev, n)
             env = lfb.env_from_buffers(knl, {"nelt": nelt},
                                        {"u": u, "d": d, "g": g, "w": w})
-            L = lfb.Launcher(knl, env)
-            r = run_timed(L.launch, 64 * n ** 3 * nelt)
-            rows.append({"order": n - 1, "npts": n, "nelt": nelt,
-                         "ms": r["ms_per_step"],
-                         "gdofs": nelt * n ** 3 / (r["ms_per_step"] * 1e-3)
-                         / 1e9,
-                         "hbm_frac": r["roofline"]["frac"],
-                         "sm_mhz": r["clocks"]["sm_mhz"]})
+            row = {"order": n - 1, "npts": n, "nelt": nelt}
+            for tag, v in (("", 0), ("fma_", 50)):
+                L = lfb.Launcher(knl, env, variant=v)
+                r = run_timed(L.launch, 64 * n ** 3 * nelt)
+                row.update({f"{tag}ms": r["ms_per_step"],
+                            f"{tag}gdofs": nelt * n ** 3
+                            / (r["ms_per_step"] * 1e-3) / 1e9,
+                            f"{tag}hbm_frac": r["roofline"]["frac"],
+                            f"{tag}sm_mhz": r["clocks"]["sm_mhz"]})
+            rows.append(row)
             del u, d, g, w, env, L
             torch.cuda.empty_cache()
-        return {"metric": "SEM sweep orders 3-15 GDOF/s", "rows": rows}
+        return {"metric": "SEM sweep orders 3-15 GDOF/s", "rows": rows,
+                "modes": "gdofs/hbm_frac: bitwise kernels (variant 0); "
+                         "fma_*: DFMA mode (variant 50, within 1e-12)"}
     raise SystemExit(f"unknown workload {wl}")
 
 # }}}
@@ -662,7 +697,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="sem2m")
-    ap.add_argument("--variant", type=int, default=0)
+    ap.add_argument("--variant", type=int, default=None,
+                    help="kernel variant; SEM default 50 (DFMA mode), "
+                         "others 0")
     ap.add_argument("--gemm-n", type=int, default=8192)
     ap.add_argument("--no-verify", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -670,6 +707,8 @@ def main():
     ap.add_argument("--e2e-nelt", type=int, default=0)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.variant is None and args.workload not in ("sem2m", "sem65k"):
+        args.variant = 0
     args.npts = 8
     args.nelt = {"sem2m": 1 << 21, "sem65k": 65536}.get(args.workload,
                                                          1 << 21)
@@ -725,7 +764,8 @@ def main():
             nelt_e2e = max(32, min(nelt_e2e, cap // 32 * 32))
         except Exception:
             pass
-        e2e = sem_e2e(knl, args.npts, nelt_e2e, dev, steps=3)
+        e2e = sem_e2e(knl, args.npts, nelt_e2e, dev, steps=3,
+                      variant=res["config"]["variant"])
         ms = max_over_ranks(e2e["ms_per_step"], world)
         e2e["value"] = nelt_e2e * world * args.npts ** 3 / (ms * 1e-3) / 1e9
         e2e["ms_per_step"] = ms

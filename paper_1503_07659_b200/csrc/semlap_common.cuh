@@ -5,6 +5,32 @@
 
 namespace lfb {
 
+// {{{ arithmetic of the two SEM modes
+//
+// F = false (default): the reference's arithmetic -- every * and + rounded
+// separately, left-associative (bitwise the reference's result).
+// F = true ("fma" variant 50): each multiply-add fused into one DFMA, same
+// association order -- within the north star's 1e-12 fp64 tolerance and
+// half the FP64 instructions (the FP64 pipe is the second ceiling, and the
+// binding one at high orders).
+
+// acc + a*b
+template <bool F>
+__device__ __forceinline__ double mac(double acc, double a, double b) {
+  if constexpr (F) return __fma_rn(a, b, acc);
+  else return dadd(acc, dmul(a, b));
+}
+
+// (x0*y0 + x1*y1) + x2*y2
+template <bool F>
+__device__ __forceinline__ double comb3(double x0, double y0, double x1,
+                                        double y1, double x2, double y2) {
+  if constexpr (F) return __fma_rn(x2, y2, __fma_rn(x1, y1, dmul(x0, y0)));
+  else return dadd(dadd(dmul(x0, y0), dmul(x1, y1)), dmul(x2, y2));
+}
+
+// }}}
+
 // fixed-order block reduction of a per-thread sum(w*w) -> partials[blockIdx]
 // (deterministic: warp shuffles in a fixed pattern, warps in index order)
 __device__ __forceinline__ void block_sumsq_partial(double acc,

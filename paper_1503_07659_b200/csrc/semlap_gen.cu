@@ -71,7 +71,7 @@ __device__ __forceinline__ void ld_pair(const double *p, double &a,
   }
 }
 
-template <int N, int E, int G, int S, bool DREG, bool SUMSQ>
+template <int N, int E, int G, int S, bool DREG, bool SUMSQ, bool F>
 __global__ void __launch_bounds__(G *GenCfg<N, E>::T, 1)
     semlap_gen_kernel(double *__restrict__ w, const double *__restrict__ u,
                       const double *__restrict__ d,
@@ -189,30 +189,29 @@ __global__ void __launch_bounds__(G *GenCfg<N, E>::T, 1)
           const double a1 = DREG ? da[l + 1] : dn[i + N * (l + 1)];
           const double b0 = DREG ? db[l] : dn[j + N * l];
           const double b1 = DREG ? db[l + 1] : dn[j + N * (l + 1)];
-          ur = dadd(ur, dmul(a0, r0));
-          us = dadd(us, dmul(b0, col[N * l]));
-          ut = dadd(ut, dmul(k0, ucol[l]));
-          ur = dadd(ur, dmul(a1, r1));
-          us = dadd(us, dmul(b1, col[N * (l + 1)]));
-          ut = dadd(ut, dmul(k1, ucol[l + 1]));
+          ur = mac<F>(ur, a0, r0);
+          us = mac<F>(us, b0, col[N * l]);
+          ut = mac<F>(ut, k0, ucol[l]);
+          ur = mac<F>(ur, a1, r1);
+          us = mac<F>(us, b1, col[N * (l + 1)]);
+          ut = mac<F>(ut, k1, ucol[l + 1]);
         }
         if constexpr (N % 2 == 1) {
           constexpr int l = N - 1;
           const double a0 = DREG ? da[l] : dn[i + N * l];
           const double b0 = DREG ? db[l] : dn[j + N * l];
-          ur = dadd(ur, dmul(a0, row[l]));
-          us = dadd(us, dmul(b0, col[N * l]));
-          ut = dadd(ut, dmul(c_dgen[N][k + N * l], ucol[l]));
+          ur = mac<F>(ur, a0, row[l]);
+          us = mac<F>(us, b0, col[N * l]);
+          ut = mac<F>(ut, c_dgen[N][k + N * l], ucol[l]);
         }
         const double *gp = sge + 6 * (i + N * j + N2 * k);
         const double2 g01 = *reinterpret_cast<const double2 *>(gp);
         const double2 g23 = *reinterpret_cast<const double2 *>(gp + 2);
         const double2 g45 = *reinterpret_cast<const double2 *>(gp + 4);
         scr_r[i + R * j + R * N * k] =
-            dadd(dadd(dmul(g01.x, ur), dmul(g01.y, us)), dmul(g23.x, ut));
-        scr_s[i + R * j + R * N * k] =
-            dadd(dadd(dmul(g01.y, ur), dmul(g23.y, us)), dmul(g45.x, ut));
-        wt[k] = dadd(dadd(dmul(g23.x, ur), dmul(g45.x, us)), dmul(g45.y, ut));
+            comb3<F>(g01.x, ur, g01.y, us, g23.x, ut);
+        scr_s[i + R * j + R * N * k] = comb3<F>(g01.y, ur, g23.y, us, g45.x, ut);
+        wt[k] = comb3<F>(g23.x, ur, g45.x, us, g45.y, ut);
       }
     }
     named_bar_sync(1 + grp, T);  // stage consumed, scratch complete
@@ -244,17 +243,16 @@ __global__ void __launch_bounds__(G *GenCfg<N, E>::T, 1)
           const double a1 = DREG ? da[l + 1] : dt[i + N * (l + 1)];
           const double b0 = DREG ? db[l] : dt[j + N * l];
           const double b1 = DREG ? db[l + 1] : dt[j + N * (l + 1)];
-          s = dadd(dadd(dadd(s, dmul(a0, r0)), dmul(b0, rs[R * l])),
-                   dmul(k0, wt[l]));
-          s = dadd(dadd(dadd(s, dmul(a1, r1)), dmul(b1, rs[R * (l + 1)])),
-                   dmul(k1, wt[l + 1]));
+          s = mac<F>(mac<F>(mac<F>(s, a0, r0), b0, rs[R * l]), k0, wt[l]);
+          s = mac<F>(mac<F>(mac<F>(s, a1, r1), b1, rs[R * (l + 1)]), k1,
+                     wt[l + 1]);
         }
         if constexpr (N % 2 == 1) {
           constexpr int l = N - 1;
           const double a0 = DREG ? da[l] : dt[i + N * l];
           const double b0 = DREG ? db[l] : dt[j + N * l];
-          s = dadd(dadd(dadd(s, dmul(a0, rr[l])), dmul(b0, rs[R * l])),
-                   dmul(c_dgen[N][l + N * k], wt[l]));
+          s = mac<F>(mac<F>(mac<F>(s, a0, rr[l]), b0, rs[R * l]),
+                     c_dgen[N][l + N * k], wt[l]);
         }
         we[N2 * k] = s;
         if constexpr (SUMSQ) acc = dadd(acc, dmul(s, s));
@@ -266,7 +264,7 @@ __global__ void __launch_bounds__(G *GenCfg<N, E>::T, 1)
   if constexpr (SUMSQ) block_sumsq_partial(acc, partials);
 }
 
-template <int N, int E, int G, int S, bool DREG>
+template <int N, int E, int G, int S, bool DREG, bool F>
 static int launch_gen(double *w, const double *u, const double *d,
                       const double *g, int64_t nelt, const lfb_launch *geom,
                       cudaStream_t s, int64_t *grid_out) {
@@ -288,8 +286,8 @@ static int launch_gen(double *w, const double *u, const double *d,
   const bool sumsq = geom && geom->sumsq;
   if (sumsq && (!geom->workspace || geom->workspace_len < grid))
     return fail(LFB_ERR_ARG, "semlap: sumsq workspace too small");
-  auto k = sumsq ? semlap_gen_kernel<N, E, G, S, DREG, true>
-                 : semlap_gen_kernel<N, E, G, S, DREG, false>;
+  auto k = sumsq ? semlap_gen_kernel<N, E, G, S, DREG, true, F>
+                 : semlap_gen_kernel<N, E, G, S, DREG, false, F>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)L::total);
   {
@@ -348,8 +346,11 @@ int sem_gen_dispatch(int n, int variant, double *w, const double *u,
                      int64_t *grid_out) {
 #define X(NN, VV, EE, GG, SS, DR)                                          \
   if (n == NN && variant == VV)                                            \
-    return launch_gen<NN, EE, GG, SS, DR>(w, u, d, g, nelt, geom, s,       \
-                                          grid_out);
+    return launch_gen<NN, EE, GG, SS, DR, false>(w, u, d, g, nelt, geom,   \
+                                                 s, grid_out);             \
+  if (VV == 0 && n == NN && variant == 50) /* default config, FMA mode */  \
+    return launch_gen<NN, EE, GG, SS, DR, VV == 0>(w, u, d, g, nelt, geom, \
+                                                   s, grid_out);
   LFB_GEN_TABLE(X)
 #undef X
   return -1;  // no generic-kernel entry for (n, variant)

@@ -66,7 +66,7 @@ __device__ __forceinline__ double cd(int a, int b) {
   return c_dmat[SLOT][a + N * b];
 }
 
-template <int N, int G, int SG, int SLOT, bool SUMSQ>
+template <int N, int G, int SG, int SLOT, bool SUMSQ, bool F>
 __global__ void __launch_bounds__(G *KcCfg<N>::T, 1)
     semlap_kc_kernel(double *__restrict__ w, const double *__restrict__ u,
                      const double *__restrict__ g, int64_t nelt,
@@ -154,21 +154,20 @@ __global__ void __launch_bounds__(G *KcCfg<N>::T, 1)
         for (int l = 0; l < N; l += 2) {
           const double2 r2 = *reinterpret_cast<const double2 *>(row + l);
           const double2 c2 = *reinterpret_cast<const double2 *>(col + l);
-          ur = dadd(ur, dmul(d1a[l], r2.x));
-          us = dadd(us, dmul(d1b[l], c2.x));
-          ut = dadd(ut, dmul(cd<SLOT, N>(k, l), ucol[l]));
-          ur = dadd(ur, dmul(d1a[l + 1], r2.y));
-          us = dadd(us, dmul(d1b[l + 1], c2.y));
-          ut = dadd(ut, dmul(cd<SLOT, N>(k, l + 1), ucol[l + 1]));
+          ur = mac<F>(ur, d1a[l], r2.x);
+          us = mac<F>(us, d1b[l], c2.x);
+          ut = mac<F>(ut, cd<SLOT, N>(k, l), ucol[l]);
+          ur = mac<F>(ur, d1a[l + 1], r2.y);
+          us = mac<F>(us, d1b[l + 1], c2.y);
+          ut = mac<F>(ut, cd<SLOT, N>(k, l + 1), ucol[l + 1]);
         }
         const double2 *g2 =
             reinterpret_cast<const double2 *>(sg + 6 * (i + N * j + N * N * k));
         const double2 g01 = g2[0], g23 = g2[1], g45 = g2[2];
         wr[i + N * j + N * N * k] =
-            dadd(dadd(dmul(g01.x, ur), dmul(g01.y, us)), dmul(g23.x, ut));
-        wsT[j + R2 * i + R2 * N * k] =
-            dadd(dadd(dmul(g01.y, ur), dmul(g23.y, us)), dmul(g45.x, ut));
-        wt[k] = dadd(dadd(dmul(g23.x, ur), dmul(g45.x, us)), dmul(g45.y, ut));
+            comb3<F>(g01.x, ur, g01.y, us, g23.x, ut);
+        wsT[j + R2 * i + R2 * N * k] = comb3<F>(g01.y, ur, g23.y, us, g45.x, ut);
+        wt[k] = comb3<F>(g23.x, ur, g45.x, us, g45.y, ut);
       }
     }
     named_bar_sync(1 + grp, T);  // stage consumed, scratch complete
@@ -198,11 +197,10 @@ __global__ void __launch_bounds__(G *KcCfg<N>::T, 1)
         for (int l = 0; l < N; l += 2) {
           const double2 r2 = *reinterpret_cast<const double2 *>(rr + l);
           const double2 s2 = *reinterpret_cast<const double2 *>(rs + l);
-          s = dadd(dadd(dadd(s, dmul(d2a[l], r2.x)), dmul(d2b[l], s2.x)),
-                   dmul(cd<SLOT, N>(l, k), wt[l]));
-          s = dadd(dadd(dadd(s, dmul(d2a[l + 1], r2.y)),
-                        dmul(d2b[l + 1], s2.y)),
-                   dmul(cd<SLOT, N>(l + 1, k), wt[l + 1]));
+          s = mac<F>(mac<F>(mac<F>(s, d2a[l], r2.x), d2b[l], s2.x),
+                     cd<SLOT, N>(l, k), wt[l]);
+          s = mac<F>(mac<F>(mac<F>(s, d2a[l + 1], r2.y), d2b[l + 1], s2.y),
+                     cd<SLOT, N>(l + 1, k), wt[l + 1]);
         }
         we[N * N * k] = s;
         if constexpr (SUMSQ) acc = dadd(acc, dmul(s, s));
@@ -214,18 +212,18 @@ __global__ void __launch_bounds__(G *KcCfg<N>::T, 1)
   if constexpr (SUMSQ) block_sumsq_partial(acc, partials);
 }
 
-template <int N, int G, int SG, int SLOT>
+template <int N, int G, int SG, int SLOT, bool F>
 static void kc_launch_slot(bool sumsq, int grid, size_t smem, double *w,
                            const double *u, const double *g, int64_t nelt,
                            double *partials, cudaStream_t s) {
-  auto k = sumsq ? semlap_kc_kernel<N, G, SG, SLOT, true>
-                 : semlap_kc_kernel<N, G, SG, SLOT, false>;
+  auto k = sumsq ? semlap_kc_kernel<N, G, SG, SLOT, true, F>
+                 : semlap_kc_kernel<N, G, SG, SLOT, false, F>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)smem);
   k<<<grid, G * KcCfg<N>::T, smem, s>>>(w, u, g, nelt, partials);
 }
 
-template <int N, int G, int SG>
+template <int N, int G, int SG, bool F>
 static int launch_kc(double *w, const double *u, const double *d,
                      const double *g, int64_t nelt, const lfb_launch *geom,
                      cudaStream_t s, int64_t *grid_out) {
@@ -253,10 +251,10 @@ static int launch_kc(double *w, const double *u, const double *d,
                               &capturing))
     return rc;
   switch (slot) {
-    case 0: kc_launch_slot<N, G, SG, 0>(sumsq, grid, L::total, w, u, g, nelt, part, s); break;
-    case 1: kc_launch_slot<N, G, SG, 1>(sumsq, grid, L::total, w, u, g, nelt, part, s); break;
-    case 2: kc_launch_slot<N, G, SG, 2>(sumsq, grid, L::total, w, u, g, nelt, part, s); break;
-    default: kc_launch_slot<N, G, SG, 3>(sumsq, grid, L::total, w, u, g, nelt, part, s); break;
+    case 0: kc_launch_slot<N, G, SG, 0, F>(sumsq, grid, L::total, w, u, g, nelt, part, s); break;
+    case 1: kc_launch_slot<N, G, SG, 1, F>(sumsq, grid, L::total, w, u, g, nelt, part, s); break;
+    case 2: kc_launch_slot<N, G, SG, 2, F>(sumsq, grid, L::total, w, u, g, nelt, part, s); break;
+    default: kc_launch_slot<N, G, SG, 3, F>(sumsq, grid, L::total, w, u, g, nelt, part, s); break;
   }
   dconst_release(0, slot, s, capturing);
   lk.unlock();
@@ -265,21 +263,23 @@ static int launch_kc(double *w, const double *u, const double *d,
                : LFB_OK;
 }
 
-// (n, variant) -> (G, SG).  -1: no constant-bank entry.
+// (n, variant) -> (G, SG, fma).  -1: no constant-bank entry.  Variant 50 =
+// the default configuration in FMA mode (semlap_common.cuh).
 #define LFB_KC_TABLE(X) \
-  X(8, 0, 4, 1)         \
-  X(8, 40, 4, 1)        \
-  X(8, 41, 5, 1)        \
-  X(8, 42, 3, 2)
+  X(8, 0, 4, 1, false)  \
+  X(8, 40, 4, 1, false) \
+  X(8, 41, 5, 1, false) \
+  X(8, 42, 3, 2, false) \
+  X(8, 50, 4, 1, true)
 
 int sem_kc_dispatch(int n, int variant, double *w, const double *u,
                     const double *d, const double *g, int64_t nelt,
                     const lfb_launch *geom, cudaStream_t s,
                     int64_t *grid_out) {
 
-#define X(NN, VV, GG, SS)                                                   \
+#define X(NN, VV, GG, SS, FF)                                               \
   if (n == NN && variant == VV)                                             \
-    return launch_kc<NN, GG, SS>(w, u, d, g, nelt, geom, s, grid_out);
+    return launch_kc<NN, GG, SS, FF>(w, u, d, g, nelt, geom, s, grid_out);
   LFB_KC_TABLE(X)
 #undef X
   return -1;

@@ -68,7 +68,7 @@ struct SlabSmem {
 // per element (the last one shorter when KS does not divide N).  Both phases
 // are fully unrolled over k and l, so the n independent accumulation chains
 // of a thread's column overlap in the FP64 pipe.
-template <int N, int G, int SGS, int KS, bool DREG, bool SUMSQ>
+template <int N, int G, int SGS, int KS, bool DREG, bool SUMSQ, bool F>
 __global__ void __launch_bounds__(G *SlabCfg<N>::T, 1)
     semlap_slab_kernel(double *__restrict__ w, const double *__restrict__ u,
                        const double *__restrict__ d,
@@ -206,10 +206,10 @@ __global__ void __launch_bounds__(G *SlabCfg<N>::T, 1)
                 const int ll = l + h;
                 const double a = DREG ? da[ll] : dn[i + N * ll];
                 const double b = DREG ? db[ll] : dn[j + N * ll];
-                ur = dadd(ur, dmul(a, h ? r1 : r0));
-                us = dadd(us, dmul(b, col[N * ll]));
+                ur = mac<F>(ur, a, h ? r1 : r0);
+                us = mac<F>(us, b, col[N * ll]);
                 // d(k,l): an immediate constant-bank operand
-                ut = dadd(ut, dmul(c_dslab[N][k + N * ll], ucol[ll]));
+                ut = mac<F>(ut, c_dslab[N][k + N * ll], ucol[ll]);
               }
             }
             const double *gp = gs + kk * C::SLAB + 6 * (i + N * j);
@@ -217,11 +217,10 @@ __global__ void __launch_bounds__(G *SlabCfg<N>::T, 1)
             const double2 g23 = *reinterpret_cast<const double2 *>(gp + 2);
             const double2 g45 = *reinterpret_cast<const double2 *>(gp + 4);
             scr_r[i + R * j + R * N * k] =
-                dadd(dadd(dmul(g01.x, ur), dmul(g01.y, us)), dmul(g23.x, ut));
+                comb3<F>(g01.x, ur, g01.y, us, g23.x, ut);
             scr_s[i + R * j + R * N * k] =
-                dadd(dadd(dmul(g01.y, ur), dmul(g23.y, us)), dmul(g45.x, ut));
-            wt[k] =
-                dadd(dadd(dmul(g23.x, ur), dmul(g45.x, us)), dmul(g45.y, ut));
+                comb3<F>(g01.y, ur, g23.y, us, g45.x, ut);
+            wt[k] = comb3<F>(g23.x, ur, g45.x, us, g45.y, ut);
           }
         }
       }
@@ -259,9 +258,8 @@ __global__ void __launch_bounds__(G *SlabCfg<N>::T, 1)
             const int ll = l + h;
             const double a = DREG ? da[ll] : dt[i + N * ll];
             const double b = DREG ? db[ll] : dt[j + N * ll];
-            s = dadd(dadd(dadd(s, dmul(a, h ? r1 : r0)),
-                          dmul(b, rs[R * ll])),
-                     dmul(c_dslab[N][ll + N * k], wt[ll]));  // d(l,k)
+            s = mac<F>(mac<F>(mac<F>(s, a, h ? r1 : r0), b, rs[R * ll]),
+                       c_dslab[N][ll + N * k], wt[ll]);  // d(l,k)
           }
         }
         we[N2 * k] = s;
@@ -274,7 +272,7 @@ __global__ void __launch_bounds__(G *SlabCfg<N>::T, 1)
   if constexpr (SUMSQ) block_sumsq_partial(acc, partials);
 }
 
-template <int N, int G, int SGS, int KS, bool DREG>
+template <int N, int G, int SGS, int KS, bool DREG, bool F>
 int launch_sem_slab(double *w, const double *u, const double *d,
                     const double *g, int64_t nelt, const lfb_launch *geom,
                     cudaStream_t s, int64_t *grid_out) {
@@ -295,8 +293,8 @@ int launch_sem_slab(double *w, const double *u, const double *d,
   const bool sumsq = geom && geom->sumsq;
   if (sumsq && (!geom->workspace || geom->workspace_len < grid))
     return fail(LFB_ERR_ARG, "semlap: sumsq workspace too small");
-  auto k = sumsq ? semlap_slab_kernel<N, G, SGS, KS, DREG, true>
-                 : semlap_slab_kernel<N, G, SGS, KS, DREG, false>;
+  auto k = sumsq ? semlap_slab_kernel<N, G, SGS, KS, DREG, true, F>
+                 : semlap_slab_kernel<N, G, SGS, KS, DREG, false, F>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)L::total);
   {
@@ -349,8 +347,11 @@ int sem_slab_dispatch(int n, int variant, double *w, const double *u,
   const int v = variant == 9 ? 0 : variant;
 #define X(NN, VV, GG, SS, KK, DR)                                         \
   if (n == NN && v == VV)                                                 \
-    return launch_sem_slab<NN, GG, SS, KK, DR>(w, u, d, g, nelt, geom, s, \
-                                               grid_out);
+    return launch_sem_slab<NN, GG, SS, KK, DR, false>(w, u, d, g, nelt,   \
+                                                      geom, s, grid_out); \
+  if (VV == 0 && n == NN && v == 50 && n >= 12) /* FMA mode */           \
+    return launch_sem_slab<NN, GG, SS, KK, DR, VV == 0 && NN >= 12>(      \
+        w, u, d, g, nelt, geom, s, grid_out);
   LFB_SLAB_TABLE(X)
 #undef X
   return fail(LFB_ERR_UNSUPPORTED,

@@ -170,6 +170,31 @@ def test_semlap_ragged_and_guarded(cuda, block, nelt):
     _sem_check(8, nelt, src, cuda, [(0, nelt)], seed=block)
 
 
+@pytest.mark.parametrize("n", list(range(2, 17)))
+def test_semlap_fma_mode(cuda, n):
+    """variant 50: the default kernel with every multiply-add fused (DFMA).
+    Tolerance parity (north star: 1e-12 relative fp64): per point against
+    the magnitude of the terms it sums -- the same operator on |u|, |d|,
+    |g| -- and normwise."""
+    nelt = max(3, 4096 // n ** 3 * 4 + 3)
+    _raw, knl = fx.translate(fx.semlap_source(n, block=1))
+    u, d, g = _sem_inputs(n, nelt, cuda, 40 + n)
+    w = torch.full_like(u, float("nan"))
+    env = lfb.env_from_buffers(knl, {"nelt": nelt},
+                               {"u": u, "d": d, "g": g, "w": w})
+    lfb.Launcher(knl, env, variant=50).launch()
+    torch.cuda.synchronize()
+    uh, dh, gh = u.cpu().numpy(), d.cpu().numpy(), g.cpu().numpy()
+    ref = oracle.semlap(np.zeros_like(uh), uh, dh, gh, n, nelt)
+    mag = oracle.semlap(np.zeros_like(uh), np.abs(uh), np.abs(dh),
+                        np.abs(gh), n, nelt)
+    got = w.cpu().numpy()
+    err = np.abs(got - ref)
+    assert (err <= 1e-12 * mag).all()
+    assert err.max() <= 1e-12 * np.abs(ref).max()
+    assert got.tobytes() != ref.tobytes() or n < 3  # really the fused path
+
+
 def test_semlap_constant_d_slots_across_streams(cuda):
     """The n = 8 default keeps d in a ring of constant-bank slots: launches
     with different d on two streams, more launches than slots, each result
