@@ -1,0 +1,370 @@
+// SEM Laplacian on the FP64 tensor cores (DMMA m8n8k4), even orders
+// n = 10..16, DFMA tolerance mode (variant 51).
+//
+// Arithmetic: the reference's operator, with every
+// multiply-add fused and the three contractions of phase 2 accumulated one
+// after the other instead of interleaved per l -- fp64 within the north
+// star's 1e-12 relative (checked per point against the magnitude of the
+// summed terms, tests/test_gpu_parity.py), not bitwise.
+//
+// Why: at high order the per-thread column kernels (semlap_gen/slab) are
+// bound by shared-memory instructions (ncu: L1 LSU pipe 72-84 %): every
+// scalar multiply-add of ur/us and of the phase-2 sums needs one operand
+// from smem, and a warp-wide LDS costs >= 2 wavefronts however few addresses
+// it reads.  As 8x8x4 matrix products the same contractions need one
+// conflict-free LDS.64 per 256 multiply-adds (the d operand stays in
+// registers), and DMMA reaches the FP64 peak with 4 warps per SM
+// (tools/micro/dmma_probe.cu: 35-37 TFLOP/s).
+//
+// Mapping (NT = 2 tiles of 8 per direction, 4 warps per element): warp
+// (it, jt) owns the 8x8 tile of points i in [8it, 8it+8), j in [8jt, 8jt+8)
+// for every k; the accumulator tiles are transposed (rows j, columns i), so
+// lane l holds (j = 8jt + l/4, i = 8it + 2(l%4) + {0,1}): two k-columns per
+// thread, adjacent in i.
+//   ur^T(:, :, k) = u(:, :, k)^T . D^T    A = u slice, B = d (registers)
+//   us^T(:, :, k) = D . u(:, :, k)^T      A = d (registers), B = u slice
+//   ut(i, j, :) = D . u(i, j, :)          the thread's own columns: DFMA with
+//                                         d(k,l) from the constant bank
+//   phase 2: w = D^T . wr + ws . D (DMMA, wr/ws from smem) + D-contraction
+//            of the thread's own wt columns (DFMA).
+// Rows / columns >= n of a tile are padding: d is zero there and the padded
+// smem is zero, so they contribute exact zeros and are never stored.
+//
+// Shared memory per element group: the u of one element and a ring of g
+// k-slabs (TMA bulk copies), a padded copy of the current u slice (row
+// stride P = 20 doubles: the fragment loads of a half warp hit 16 distinct
+// 8-byte bank slots), and wr / ws for the whole element in the same padded
+// layout.
+#include "dconst.cuh"
+#include "lfb_common.cuh"
+#include "semlap_common.cuh"
+
+namespace lfb {
+
+__constant__ double c_dtc[17][256];  // d(a,b) at [N][a + N b]
+
+template <int N>
+struct TcCfg {
+  static constexpr int NT = 2;               // 8-wide tiles per direction
+  static constexpr int W = NT * NT;          // warps per element
+  static constexpr int T = 32 * W;
+  static constexpr int KT = (N + 3) / 4;     // k-steps of 4
+  static constexpr int P = 8 * NT + 4;       // padded row stride (20)
+  static constexpr int B = 8 * NT;           // padded column extent (16)
+  static constexpr int NP = N * N * N;
+  static constexpr int SL = P * B;           // one padded slice
+  static constexpr int SLAB = 6 * N * N;     // g of one k-slice
+};
+
+template <int N, int G, int SGS, int KS>
+struct TcSmem {
+  using C = TcCfg<N>;
+  static constexpr size_t bars = 256;
+  static constexpr size_t grp_doubles =
+      (size_t)C::NP + (size_t)SGS * KS * C::SLAB + 3 * (size_t)C::SL * N;
+  static constexpr size_t grp_bytes = (grp_doubles * 8 + 127) / 128 * 128;
+  static constexpr size_t total = bars + G * grp_bytes;
+};
+
+// D = A(8x4, row) * B(4x8, col) + D; lane l holds a = A[l/4][l%4],
+// b = B[l%4][l/4], d = D[l/4][2(l%4) + {0,1}]
+__device__ __forceinline__ void dmma(double &d0, double &d1, double a,
+                                     double b) {
+  asm volatile(
+      "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, "
+      "{%0,%1};"
+      : "+d"(d0), "+d"(d1)
+      : "d"(a), "d"(b));
+}
+
+template <int N>
+__device__ __forceinline__ double dtc(int a, int b) {  // d(a,b), 0 outside
+  return (a < N && b < N) ? c_dtc[N][a + N * b] : 0.0;
+}
+
+template <int N, int G, int SGS, int KS, bool SUMSQ>
+__global__ void __launch_bounds__(G *TcCfg<N>::T, 1)
+    semlap_tc_kernel(double *__restrict__ w, const double *__restrict__ u,
+                     const double *__restrict__ g, int64_t nelt,
+                     double *__restrict__ partials) {
+  using C = TcCfg<N>;
+  using L = TcSmem<N, G, SGS, KS>;
+  constexpr int NP = C::NP, T = C::T, KT = C::KT, P = C::P, SL = C::SL;
+  constexpr int N2 = N * N;
+  static_assert(N % 2 == 0 && N > 8 && N <= 16, "even n = 10..16");
+  static_assert(G * (1 + SGS) <= 32, "mbarriers");
+
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t *bars = reinterpret_cast<uint64_t *>(smem);
+
+  const int tid = threadIdx.x;
+  const int grp = tid / T;
+  const int lt = tid % T;
+  const int warp = lt / 32, lane = lt % 32;
+  const int it = warp / C::NT, jt = warp % C::NT;
+  const int r = lane / 4, q = lane % 4;
+  // accumulator rows = j, columns = i: the two points of a thread are
+  // adjacent in i (one 16-byte store of w) and the g reads of a quarter
+  // warp spread over the banks
+  const int j = 8 * jt + r;
+  const int i0 = 8 * it + 2 * q;       // accumulator columns i0, i0 + 1
+  const bool vj = j < N;
+  const bool v0 = vj && i0 < N, v1 = vj && i0 + 1 < N;
+
+  double *gb = reinterpret_cast<double *>(smem + L::bars +
+                                          (size_t)grp * L::grp_bytes);
+  double *ust = gb;                          // u of the element (NP)
+  double *slabs = ust + NP;                  // SGS x KS x 6 N^2
+  double *upd = slabs + SGS * KS * C::SLAB;  // u: N padded slices
+  double *wrp = upd + (size_t)SL * N;        // wr: N padded slices
+  double *wsp = wrp + (size_t)SL * N;        // ws: N padded slices
+  uint64_t *ubar = bars + grp * (1 + SGS);
+  uint64_t *gbar = ubar + 1;
+
+  const int64_t q0 = (int64_t)blockIdx.x * G + grp;
+  const int64_t Q = (int64_t)gridDim.x * G;
+  const int64_t mine = nelt > q0 ? (nelt - q0 + Q - 1) / Q : 0;
+  auto elem = [&](int64_t m) -> int64_t { return q0 + m * Q; };
+
+  if (tid == 0) {
+    for (int x = 0; x < G * (1 + SGS); ++x) mbar_init(&bars[x], 1);
+    fence_mbar_init();
+  }
+  // zero the padded buffers once: padding stays zero for the whole kernel
+  for (int x = lt; x < 3 * SL * N; x += T) upd[x] = 0.0;
+  __syncthreads();
+
+  const uint64_t pol = policy_evict_first();
+  auto issue_u = [&](int64_t m) {
+    mbar_arrive_expect_tx(ubar, NP * 8);
+    bulk_g2s_stream(ust, u + elem(m) * NP, NP * 8, ubar, pol);
+  };
+  // slab q = KS consecutive k-slices of g (q = m * N / KS + k / KS)
+  static_assert(N % KS == 0, "KS divides n");
+  auto issue_slab = [&](int64_t sq) {
+    const int64_t e = elem(sq / (N / KS));
+    const int k0 = (int)(sq % (N / KS)) * KS;
+    const int slot = (int)(sq % SGS);
+    mbar_arrive_expect_tx(&gbar[slot], (uint32_t)(KS * C::SLAB * 8));
+    bulk_g2s_stream(slabs + (size_t)slot * KS * C::SLAB,
+                    g + e * 6 * NP + (int64_t)k0 * 6 * N2, KS * C::SLAB * 8,
+                    &gbar[slot], pol);
+  };
+  const int64_t nslabs = mine * (N / KS);
+  if (lt == 0) {
+    if (mine > 0) issue_u(0);
+    for (int64_t s = 0; s < SGS && s < nslabs; ++s) issue_slab(s);
+  }
+
+  // d fragments (registers for the whole kernel):
+  //   ur : A = d(i, l)       a = d(8it + r, 4ks + q)
+  //   us : B = d(j, l)^T     b = d(8jt + r, 4ks + q)   [B[l][j] = d(j,l)]
+  //   w1 : A = d(l, i)^T     a = d(4ks + q, 8it + r)
+  //   w2 : B = d(l, j)       b = d(4ks + q, 8jt + r)
+  double fa_r[KT], fb_s[KT], fa_t[KT], fb_t[KT];
+#pragma unroll
+  for (int ks = 0; ks < KT; ++ks) {
+    fa_r[ks] = dtc<N>(8 * it + r, 4 * ks + q);
+    fb_s[ks] = dtc<N>(8 * jt + r, 4 * ks + q);
+    fa_t[ks] = dtc<N>(4 * ks + q, 8 * it + r);
+    fb_t[ks] = dtc<N>(4 * ks + q, 8 * jt + r);
+  }
+
+  double acc_sq = 0.0;
+  for (int64_t m = 0; m < mine; ++m) {
+    const int64_t e = elem(m);
+    mbar_wait(ubar, (uint32_t)(m & 1));
+
+    // padded copy of the whole element: u(a, b, k) at a + P b + SL k
+    for (int x = lt; x < NP; x += T) {
+      const int a = x % N, b = (x / N) % N, k = x / N2;
+      upd[a + P * b + SL * k] = ust[x];
+    }
+    // the thread's own two k-columns u(i, j0 + c, :) -> ut for every k:
+    // 2N independent DFMA chains (d(k,l) are constant-bank operands)
+    double t0[N], t1[N];
+    {
+      double uc0[N], uc1[N];
+#pragma unroll
+      for (int l = 0; l < N; ++l) {
+        uc0[l] = v0 ? ust[i0 + N * j + N2 * l] : 0.0;
+        uc1[l] = v1 ? ust[i0 + 1 + N * j + N2 * l] : 0.0;
+      }
+#pragma unroll
+      for (int k = 0; k < N; ++k) t0[k] = t1[k] = 0.0;
+#pragma unroll
+      for (int l = 0; l < N; ++l) {
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+          const double dk = c_dtc[N][k + N * l];
+          t0[k] = __fma_rn(dk, uc0[l], t0[k]);
+          t1[k] = __fma_rn(dk, uc1[l], t1[k]);
+        }
+      }
+    }
+    named_bar_sync(1 + grp, T);  // padded u complete, u stage consumed
+    if (lt == 0 && m + 1 < mine) {
+      fence_proxy_async_smem();
+      issue_u(m + 1);  // overlaps both phases of this element
+    }
+
+    // ---- phase 1: ur / us on the tensor cores, combine with g
+    double wt0[N], wt1[N];
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      const int64_t s = m * N + k;
+      const double *sl = upd + SL * k;
+      double r0 = 0.0, r1 = 0.0, s0 = 0.0, s1 = 0.0;
+#pragma unroll
+      for (int ks = 0; ks < KT; ++ks) {
+        // ur^T: A[j][l] = u(l, j, k) at l + P j, B[l][i] = d(i, l)
+        dmma(r0, r1, sl[(4 * ks + q) + P * (8 * jt + r)], fa_r[ks]);
+        // us^T: A[j][l] = d(j, l), B[l][i] = u(i, l, k) at i + P l
+        dmma(s0, s1, fb_s[ks], sl[(8 * it + r) + P * (4 * ks + q)]);
+      }
+      if (k % KS == 0) mbar_wait(&gbar[(s / KS) % SGS],
+                                 (uint32_t)((s / KS / SGS) & 1));
+      // combine with g at (i, j0 + c, k)
+      const double *gs = slabs + (size_t)((s / KS) % SGS) * KS * C::SLAB +
+                         (size_t)(k % KS) * C::SLAB;
+      double *wr_k = wrp + (size_t)SL * k;
+      double *ws_k = wsp + (size_t)SL * k;
+      if (v0) {
+        const double2 *g2 =
+            reinterpret_cast<const double2 *>(gs + 6 * (i0 + N * j));
+        const double2 g01 = g2[0], g23 = g2[1], g45 = g2[2];
+        wr_k[i0 + P * j] = comb3<true>(g01.x, r0, g01.y, s0, g23.x, t0[k]);
+        ws_k[i0 + P * j] = comb3<true>(g01.y, r0, g23.y, s0, g45.x, t0[k]);
+        wt0[k] = comb3<true>(g23.x, r0, g45.x, s0, g45.y, t0[k]);
+      } else {
+        wt0[k] = 0.0;
+      }
+      if (v1) {
+        const double2 *g2 =
+            reinterpret_cast<const double2 *>(gs + 6 * (i0 + 1 + N * j));
+        const double2 g01 = g2[0], g23 = g2[1], g45 = g2[2];
+        wr_k[i0 + 1 + P * j] =
+            comb3<true>(g01.x, r1, g01.y, s1, g23.x, t1[k]);
+        ws_k[i0 + 1 + P * j] =
+            comb3<true>(g01.y, r1, g23.y, s1, g45.x, t1[k]);
+        wt1[k] = comb3<true>(g23.x, r1, g45.x, s1, g45.y, t1[k]);
+      } else {
+        wt1[k] = 0.0;
+      }
+      if (k % KS == KS - 1 || k == N - 1) {
+        named_bar_sync(1 + grp, T);  // slab consumed
+        const int64_t slab = s / KS;
+        if (lt == 0 && slab + SGS < nslabs) {
+          fence_proxy_async_smem();
+          issue_slab(slab + SGS);
+        }
+      }
+    }
+    // the own-column contraction of phase 2 for every k (2N chains),
+    // the starting value of the tensor-core sums below
+#pragma unroll
+    for (int k = 0; k < N; ++k) t0[k] = t1[k] = 0.0;
+#pragma unroll
+    for (int l = 0; l < N; ++l) {
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        const double dk = c_dtc[N][l + N * k];
+        t0[k] = __fma_rn(dk, wt0[l], t0[k]);
+        t1[k] = __fma_rn(dk, wt1[l], t1[k]);
+      }
+    }
+    // (the last slab barrier above made wr / ws complete)
+
+    // ---- phase 2
+    double *we = w + e * NP;
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      const double *wr_k = wrp + (size_t)SL * k;
+      const double *ws_k = wsp + (size_t)SL * k;
+      double a0 = t0[k], a1 = t1[k];
+#pragma unroll
+      for (int ks = 0; ks < KT; ++ks) {
+        // sum_l d(l,i) wr(l,j,k): A[j][l] = wr(l,j,k), B[l][i] = d(l,i)
+        dmma(a0, a1, wr_k[(4 * ks + q) + P * (8 * jt + r)], fa_t[ks]);
+        // sum_l ws(i,l,k) d(l,j): A[j][l] = d(l,j), B[l][i] = ws(i,l,k)
+        dmma(a0, a1, fb_t[ks], ws_k[(8 * it + r) + P * (4 * ks + q)]);
+      }
+      if (v1) {
+        *reinterpret_cast<double2 *>(we + i0 + N * j + N2 * k) =
+            make_double2(a0, a1);
+      } else if (v0) {
+        we[i0 + N * j + N2 * k] = a0;
+      }
+      if constexpr (SUMSQ) {
+        if (v0) acc_sq = dadd(acc_sq, dmul(a0, a0));
+        if (v1) acc_sq = dadd(acc_sq, dmul(a1, a1));
+      }
+    }
+    named_bar_sync(1 + grp, T);  // wr / ws / padded u reads done
+  }
+
+  if constexpr (SUMSQ) block_sumsq_partial(acc_sq, partials);
+}
+
+template <int N, int G, int SGS, int KS>
+static int launch_tc(double *w, const double *u, const double *d,
+                     const double *g, int64_t nelt, const lfb_launch *geom,
+                     cudaStream_t s, int64_t *grid_out) {
+  using L = TcSmem<N, G, SGS, KS>;
+  static_assert(L::total <= 227 * 1024, "smem");
+  int sms = sm_count(geom);
+  if (sms <= 0) sms = 148;
+  const int per_sm = (geom && geom->ctas_per_sm > 0) ? geom->ctas_per_sm : 1;
+  int64_t grid64 = (int64_t)sms * per_sm;
+  if (grid64 * G > nelt) grid64 = (nelt + G - 1) / G;
+  const int grid = (int)(grid64 < 1 ? 1 : grid64);
+  if (grid_out) {
+    *grid_out = grid;
+    return LFB_OK;
+  }
+  const bool sumsq = geom && geom->sumsq;
+  if (sumsq && (!geom->workspace || geom->workspace_len < grid))
+    return fail(LFB_ERR_ARG, "semlap: sumsq workspace too small");
+  if (!aligned(u, 16) || !aligned(g, 16))
+    return fail(LFB_ERR_UNSUPPORTED, "semlap(tc): u, g not 16-byte aligned");
+  auto k = sumsq ? semlap_tc_kernel<N, G, SGS, KS, true>
+                 : semlap_tc_kernel<N, G, SGS, KS, false>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)L::total);
+  {
+    std::unique_lock<std::mutex> lk;
+    bool capturing = false;
+    int slot = N;
+    if (int rc = dconst_acquire(c_dtc, 256 * 8, 3, &slot, d, N, s, &lk,
+                                &capturing))
+      return rc;
+    k<<<grid, G * TcCfg<N>::T, L::total, s>>>(
+        w, u, g, nelt, sumsq ? geom->workspace : nullptr);
+    dconst_release(3, slot, s, capturing);
+  }
+  if (int rc = check_launch("lfb_semlap_f64(dmma)")) return rc;
+  return sumsq ? sem_sumsq_finish(geom->workspace, grid, geom->sumsq, s)
+               : LFB_OK;
+}
+
+// (n, variant) -> (groups per CTA, g-slab ring depth, k-slices per slab).  Variant 51: the
+// DMMA kernel; -1 when there is none for n.
+#define LFB_TC_TABLE(X) \
+  X(10, 51, 2, 2, 2)    \
+  X(12, 51, 1, 3, 2)    \
+  X(14, 51, 1, 2, 2)    \
+  X(16, 51, 1, 2, 2)
+
+int sem_tc_dispatch(int n, int variant, double *w, const double *u,
+                    const double *d, const double *g, int64_t nelt,
+                    const lfb_launch *geom, cudaStream_t s,
+                    int64_t *grid_out) {
+#define X(NN, VV, GG, SS, KK)                                               \
+  if (n == NN && variant == VV)                                             \
+    return launch_tc<NN, GG, SS, KK>(w, u, d, g, nelt, geom, s, grid_out);
+  LFB_TC_TABLE(X)
+#undef X
+  return -1;
+}
+
+}  // namespace lfb

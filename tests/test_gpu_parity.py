@@ -170,9 +170,11 @@ def test_semlap_ragged_and_guarded(cuda, block, nelt):
     _sem_check(8, nelt, src, cuda, [(0, nelt)], seed=block)
 
 
-@pytest.mark.parametrize("n", list(range(2, 17)))
-def test_semlap_fma_mode(cuda, n):
-    """variant 50: the default kernel with every multiply-add fused (DFMA).
+@pytest.mark.parametrize("n,variant", [(n, 50) for n in range(2, 17)]
+                         + [(n, 51) for n in (10, 12, 14, 16)])
+def test_semlap_fma_mode(cuda, n, variant):
+    """variant 50: the default kernel with every multiply-add fused (DFMA);
+    variant 51: the FP64 tensor-core (DMMA) kernel for even n >= 10.
     Tolerance parity (north star: 1e-12 relative fp64): per point against
     the magnitude of the terms it sums -- the same operator on |u|, |d|,
     |g| -- and normwise."""
@@ -182,7 +184,7 @@ def test_semlap_fma_mode(cuda, n):
     w = torch.full_like(u, float("nan"))
     env = lfb.env_from_buffers(knl, {"nelt": nelt},
                                {"u": u, "d": d, "g": g, "w": w})
-    lfb.Launcher(knl, env, variant=50).launch()
+    lfb.Launcher(knl, env, variant=variant).launch()
     torch.cuda.synchronize()
     uh, dh, gh = u.cpu().numpy(), d.cpu().numpy(), g.cpu().numpy()
     ref = oracle.semlap(np.zeros_like(uh), uh, dh, gh, n, nelt)
