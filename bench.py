@@ -132,11 +132,21 @@ def dist_init(n_gpus):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1 and world != n_gpus:
         raise SystemExit(f"--gpus {n_gpus} but WORLD_SIZE={world}")
+    # test hooks: LFB_BENCH_ONE_DEVICE=1 puts every rank on cuda:0 and
+    # LFB_BENCH_BACKEND=gloo replaces NCCL (NCCL refuses two ranks on one
+    # GPU) -- exercises the multi-rank path on a one-GPU box; such numbers
+    # are not measurements
+    if os.environ.get("LFB_BENCH_ONE_DEVICE") == "1":
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl",
-                                device_id=torch.device("cuda", local))
+        backend = os.environ.get("LFB_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl",
+                                    device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     return rank, world, local
 
 
@@ -306,7 +316,11 @@ def sem_bench(args, rank, world, local):
                    "oracle in verify and tests)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": _traffic(f"semlap_n{n}"),
+                     # DRAM bytes of the committed 2^21-element capture,
+                     # scaled to this rank's elements
+                     "traffic": (None if _traffic(f"semlap_n{n}") is None
+                                 else _traffic(f"semlap_n{n}") * nelt
+                                 / (1 << 21)),
                      "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": bytes_per_launch,
                      "kernel": f"semlap_kc_kernel variant {sem_variant} "

@@ -10,6 +10,7 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 import oracle
+from conftest import REPO
 from paper_1503_07659_b200.dist import (allreduce_max, allreduce_sum,
                                         shard_params, shard_range)
 
@@ -79,3 +80,29 @@ def test_gloo_world2_norm_allreduce():
     for _rank, total, worst in res:
         assert abs(total - want) <= 1e-12 * want
         assert worst == world - 1
+
+
+@pytest.mark.gpu
+def test_bench_multi_rank_path_on_one_gpu(tmp_path):
+    """bench.py under torchrun with 2 ranks (both on cuda:0, gloo -- NCCL
+    refuses two ranks on one GPU): element shards, barriers, max over ranks,
+    the all-reduced verification norm and one JSON line from rank 0."""
+    import json
+    import subprocess
+    import sys
+    env = dict(os.environ, LFB_BENCH_ONE_DEVICE="1", LFB_BENCH_BACKEND="gloo")
+    r = subprocess.run(
+        [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+         "--nproc-per-node", "2", "--master-addr", "127.0.0.1",
+         "--master-port", "29541", os.path.join(REPO, "bench.py"),
+         "--gpus", "2", "--workload", "sem65k", "--steps", "3",
+         "--warmup", "3", "--no-cpu", "--e2e-nelt", "4096"],
+        capture_output=True, text=True, timeout=900, env=env, cwd=REPO)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1  # rank 0 only
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0
+    assert d["verify"]["max_err_over_magnitude_head"] <= 1e-12
+    assert d["verify"]["max_err_over_magnitude_tail"] <= 1e-12
+    assert d["e2e"]["value"] > 0
