@@ -21,6 +21,19 @@ __device__ __forceinline__ double mac(double acc, double a, double b) {
   else return dadd(acc, dmul(a, b));
 }
 
+// 0 + a*b, the first step of every accumulation chain.  The reference adds
+// the product to the literal 0; that addition only changes a -0 product
+// into +0, so the bitwise mode does it with two integer instructions
+// instead of a DADD (3.6 % of the operator's FP64 instructions at n = 8).
+template <bool F>
+__device__ __forceinline__ double mac0(double a, double b) {
+  const double p = dmul(a, b);
+  if constexpr (F) return p;
+  const long long bits = __double_as_longlong(p);
+  return __longlong_as_double(bits == (long long)0x8000000000000000ULL
+                                  ? 0LL : bits);
+}
+
 // (x0*y0 + x1*y1) + x2*y2
 template <bool F>
 __device__ __forceinline__ double comb3(double x0, double y0, double x1,

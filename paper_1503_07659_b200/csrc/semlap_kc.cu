@@ -147,16 +147,22 @@ __global__ void __launch_bounds__(G *KcCfg<N>::T, 1)
       }
 #pragma unroll
       for (int k = 0; k < N; ++k) {
-        double ur = 0.0, us = 0.0, ut = 0.0;
+        double ur, us, ut;
         const double *row = su + N * j + N * N * k;    // u(.,j,k)
         const double *col = uT + R2 * i + R2 * N * k;  // u(i,.,k)
 #pragma unroll
         for (int l = 0; l < N; l += 2) {
           const double2 r2 = *reinterpret_cast<const double2 *>(row + l);
           const double2 c2 = *reinterpret_cast<const double2 *>(col + l);
-          ur = mac<F>(ur, d1a[l], r2.x);
-          us = mac<F>(us, d1b[l], c2.x);
-          ut = mac<F>(ut, cd<SLOT, N>(k, l), ucol[l]);
+          if (l == 0) {  // ur = 0 + d*u ... (the reference's s = 0 start)
+            ur = mac0<F>(d1a[0], r2.x);
+            us = mac0<F>(d1b[0], c2.x);
+            ut = mac0<F>(cd<SLOT, N>(k, 0), ucol[0]);
+          } else {
+            ur = mac<F>(ur, d1a[l], r2.x);
+            us = mac<F>(us, d1b[l], c2.x);
+            ut = mac<F>(ut, cd<SLOT, N>(k, l), ucol[l]);
+          }
           ur = mac<F>(ur, d1a[l + 1], r2.y);
           us = mac<F>(us, d1b[l + 1], c2.y);
           ut = mac<F>(ut, cd<SLOT, N>(k, l + 1), ucol[l + 1]);
@@ -192,12 +198,14 @@ __global__ void __launch_bounds__(G *KcCfg<N>::T, 1)
       for (int k = 0; k < N; ++k) {
         const double *rr = wr + R1 * j + N * N * k;    // wr(.,j,k)
         const double *rs = wsT + R2 * i + R2 * N * k;  // ws(i,.,k)
-        double s = 0.0;
+        double s;
 #pragma unroll
         for (int l = 0; l < N; l += 2) {
           const double2 r2 = *reinterpret_cast<const double2 *>(rr + l);
           const double2 s2 = *reinterpret_cast<const double2 *>(rs + l);
-          s = mac<F>(mac<F>(mac<F>(s, d2a[l], r2.x), d2b[l], s2.x),
+          s = mac<F>(mac<F>(l == 0 ? mac0<F>(d2a[0], r2.x)
+                                   : mac<F>(s, d2a[l], r2.x),
+                            d2b[l], s2.x),
                      cd<SLOT, N>(l, k), wt[l]);
           s = mac<F>(mac<F>(mac<F>(s, d2a[l + 1], r2.y), d2b[l + 1], s2.y),
                      cd<SLOT, N>(l + 1, k), wt[l + 1]);
