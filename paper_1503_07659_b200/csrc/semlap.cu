@@ -607,9 +607,10 @@ static int sem_dispatch(double *w, const double *u, const double *d,
                                    grid_out);
     if (rc != -1) return rc;
   }
-  if (var0 == 51 || (var0 == 50 && n == 16)) {
-    // FP64 tensor cores (semlap_tc.cu), even n = 10..16; the DFMA-mode
-    // default at n = 16, where it beats the column kernels (58 % vs 53 %)
+  if (var0 == 51 || (var0 == 50 && n >= 15)) {
+    // FP64 tensor cores (semlap_tc.cu), n = 9..16; the DFMA-mode default
+    // at n = 15, 16, where it beats the column kernels (n = 15: 49 % vs
+    // 38 % of HBM)
     const int rc = sem_tc_dispatch(n, 51, w, u, d, g, nelt, geom, s,
                                    grid_out);
     if (rc != -1) return rc;

@@ -1,5 +1,5 @@
-// SEM Laplacian on the FP64 tensor cores (DMMA m8n8k4), even orders
-// n = 10..16, DFMA tolerance mode (variant 51).
+// SEM Laplacian on the FP64 tensor cores (DMMA m8n8k4), n = 9..16, DFMA
+// tolerance mode (variant 51).
 //
 // Arithmetic: the reference's operator, with every
 // multiply-add fused and the three contractions of phase 2 accumulated one
@@ -52,6 +52,7 @@ struct TcCfg {
   static constexpr int P = 8 * NT + 4;       // padded row stride (20)
   static constexpr int B = 8 * NT;           // padded column extent (16)
   static constexpr int NP = N * N * N;
+  static constexpr int UST = (NP + 2 + 1) / 2 * 2;  // + 8-byte lead, even
   static constexpr int SL = P * B;           // one padded slice
   static constexpr int SLAB = 6 * N * N;     // g of one k-slice
 };
@@ -61,7 +62,7 @@ struct TcSmem {
   using C = TcCfg<N>;
   static constexpr size_t bars = 256;
   static constexpr size_t grp_doubles =
-      (size_t)C::NP + (size_t)SGS * KS * C::SLAB + 3 * (size_t)C::SL * N;
+      (size_t)C::UST + (size_t)SGS * KS * C::SLAB + 3 * (size_t)C::SL * N;
   static constexpr size_t grp_bytes = (grp_doubles * 8 + 127) / 128 * 128;
   static constexpr size_t total = bars + G * grp_bytes;
 };
@@ -91,7 +92,7 @@ __global__ void __launch_bounds__(G *TcCfg<N>::T, 1)
   using L = TcSmem<N, G, SGS, KS>;
   constexpr int NP = C::NP, T = C::T, KT = C::KT, P = C::P, SL = C::SL;
   constexpr int N2 = N * N;
-  static_assert(N % 2 == 0 && N > 8 && N <= 16, "even n = 10..16");
+  static_assert(N > 8 && N <= 16, "n = 9..16");
   static_assert(G * (1 + SGS) <= 32, "mbarriers");
 
   extern __shared__ __align__(128) unsigned char smem[];
@@ -113,8 +114,8 @@ __global__ void __launch_bounds__(G *TcCfg<N>::T, 1)
 
   double *gb = reinterpret_cast<double *>(smem + L::bars +
                                           (size_t)grp * L::grp_bytes);
-  double *ust = gb;                          // u of the element (NP)
-  double *slabs = ust + NP;                  // SGS x KS x 6 N^2
+  double *ust0 = gb;                         // u of the element (UST)
+  double *slabs = ust0 + C::UST;             // SGS x KS x 6 N^2
   double *upd = slabs + SGS * KS * C::SLAB;  // u: N padded slices
   double *wrp = upd + (size_t)SL * N;        // wr: N padded slices
   double *wsp = wrp + (size_t)SL * N;        // ws: N padded slices
@@ -135,12 +136,29 @@ __global__ void __launch_bounds__(G *TcCfg<N>::T, 1)
   __syncthreads();
 
   const uint64_t pol = policy_evict_first();
+  // u of element e: bulk copy of the 16-byte aligned superset (odd n: the
+  // element starts 8 bytes into it for odd e); a final element whose
+  // rounded end would run past the array is copied by the threads
+  const int64_t u_bytes_total = nelt * NP * 8;
+  auto u_lead = [&](int64_t e) -> int { return (int)((e * NP) & 1); };
+  auto u_span = [&](int64_t e) -> int64_t {
+    return ((int64_t)(u_lead(e) + NP) * 8 + 15) / 16 * 16;
+  };
+  auto u_bulk_ok = [&](int64_t e) -> bool {
+    return (e * NP - u_lead(e)) * 8 + u_span(e) <= u_bytes_total;
+  };
   auto issue_u = [&](int64_t m) {
-    mbar_arrive_expect_tx(ubar, NP * 8);
-    bulk_g2s_stream(ust, u + elem(m) * NP, NP * 8, ubar, pol);
+    const int64_t e = elem(m);
+    if (u_bulk_ok(e)) {
+      mbar_arrive_expect_tx(ubar, (uint32_t)u_span(e));
+      bulk_g2s_stream(ust0, u + e * NP - u_lead(e), (uint32_t)u_span(e),
+                      ubar, pol);
+    } else {
+      mbar_arrive_expect_tx(ubar, 0);
+    }
   };
   // slab q = KS consecutive k-slices of g (q = m * N / KS + k / KS)
-  static_assert(N % KS == 0, "KS divides n");
+  static_assert(N % KS == 0, "KS divides n");  // odd n: KS = 1
   auto issue_slab = [&](int64_t sq) {
     const int64_t e = elem(sq / (N / KS));
     const int k0 = (int)(sq % (N / KS)) * KS;
@@ -174,6 +192,11 @@ __global__ void __launch_bounds__(G *TcCfg<N>::T, 1)
   for (int64_t m = 0; m < mine; ++m) {
     const int64_t e = elem(m);
     mbar_wait(ubar, (uint32_t)(m & 1));
+    const double *ust = ust0 + u_lead(e);
+    if (!u_bulk_ok(e)) {
+      for (int x = lt; x < NP; x += T) ust0[u_lead(e) + x] = u[e * NP + x];
+      named_bar_sync(1 + grp, T);
+    }
 
     // padded copy of the whole element: u(a, b, k) at a + P b + SL k
     for (int x = lt; x < NP; x += T) {
@@ -289,11 +312,12 @@ __global__ void __launch_bounds__(G *TcCfg<N>::T, 1)
         // sum_l ws(i,l,k) d(l,j): A[j][l] = d(l,j), B[l][i] = ws(i,l,k)
         dmma(a0, a1, fb_t[ks], ws_k[(8 * it + r) + P * (4 * ks + q)]);
       }
-      if (v1) {
+      if (N % 2 == 0 && v1) {  // even n: 16-byte aligned pair
         *reinterpret_cast<double2 *>(we + i0 + N * j + N2 * k) =
             make_double2(a0, a1);
-      } else if (v0) {
-        we[i0 + N * j + N2 * k] = a0;
+      } else {
+        if (v0) we[i0 + N * j + N2 * k] = a0;
+        if (v1) we[i0 + 1 + N * j + N2 * k] = a1;
       }
       if constexpr (SUMSQ) {
         if (v0) acc_sq = dadd(acc_sq, dmul(a0, a0));
@@ -350,9 +374,13 @@ static int launch_tc(double *w, const double *u, const double *d,
 // (n, variant) -> (groups per CTA, g-slab ring depth, k-slices per slab).  Variant 51: the
 // DMMA kernel; -1 when there is none for n.
 #define LFB_TC_TABLE(X) \
+  X(9, 51, 2, 3, 1)     \
   X(10, 51, 2, 2, 2)    \
+  X(11, 51, 1, 4, 1)    \
   X(12, 51, 1, 3, 2)    \
+  X(13, 51, 1, 4, 1)    \
   X(14, 51, 1, 2, 2)    \
+  X(15, 51, 1, 4, 1)    \
   X(16, 51, 1, 2, 2)
 
 int sem_tc_dispatch(int n, int variant, double *w, const double *u,
