@@ -31,8 +31,8 @@ struct DConstRing {
 };
 
 inline DConstRing &dconst_ring(int tag, int dev) {
-  static DConstRing rings[4][16];
-  return rings[tag & 3][dev & 15];
+  static DConstRing rings[8][16];
+  return rings[tag & 7][dev & 15];
 }
 
 // Copies d (n*n doubles, device memory) to `symbol` at byte offset

@@ -607,6 +607,14 @@ static int sem_dispatch(double *w, const double *u, const double *d,
                                    grid_out);
     if (rc != -1) return rc;
   }
+  if (var0 == 60 || var0 == 61 ||
+      (var0 == 50 && (n == 7 || n == 9 || n == 10))) {
+    // two k-columns per thread (semlap_gen2.cu), n = 7, 9..12; the DFMA-mode
+    // default at n = 7, 9, 10 (+2..6 % over one column per thread)
+    const int rc = sem_gen2_dispatch(n, var0 == 50 ? 61 : var0, w, u, d, g,
+                                     nelt, geom, s, grid_out);
+    if (rc != -1) return rc;
+  }
   if (var0 == 51 || (var0 == 50 && n >= 15)) {
     // FP64 tensor cores (semlap_tc.cu), n = 9..16; the DFMA-mode default
     // at n = 15, 16, where it beats the column kernels (n = 15: 49 % vs

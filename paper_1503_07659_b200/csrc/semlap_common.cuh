@@ -72,6 +72,12 @@ int sem_gen_dispatch(int n, int variant, double *w, const double *u,
                      const lfb_launch *geom, cudaStream_t s,
                      int64_t *grid_out);
 
+// -1 when the two-columns-per-thread kernel has no entry for (n, variant)
+int sem_gen2_dispatch(int n, int variant, double *w, const double *u,
+                      const double *d, const double *g, int64_t nelt,
+                      const lfb_launch *geom, cudaStream_t s,
+                      int64_t *grid_out);
+
 // -1 when the DMMA kernel has no entry for (n, variant)
 int sem_tc_dispatch(int n, int variant, double *w, const double *u,
                     const double *d, const double *g, int64_t nelt,

@@ -119,7 +119,7 @@ def test_semlap_orders(cuda, n):
 GEN_VARIANTS = [(4, 20), (4, 21), (5, 20), (5, 21), (5, 22), (6, 20),
                 (6, 21), (6, 22), (7, 20), (7, 21), (7, 22), (8, 20),
                 (8, 21), (8, 22), (9, 20), (9, 21), (10, 20), (10, 21),
-                (11, 20)]
+                (11, 20), (7, 60), (9, 60), (10, 60), (11, 60), (12, 60)]
 
 
 @pytest.mark.parametrize("n,variant", GEN_VARIANTS)
@@ -171,7 +171,8 @@ def test_semlap_ragged_and_guarded(cuda, block, nelt):
 
 
 @pytest.mark.parametrize("n,variant", [(n, 50) for n in range(2, 17)]
-                         + [(n, 51) for n in range(9, 17)])
+                         + [(n, 51) for n in range(9, 17)]
+                         + [(n, 61) for n in (7, 9, 10, 11, 12)])
 def test_semlap_fma_mode(cuda, n, variant):
     """variant 50: the default kernel with every multiply-add fused (DFMA);
     variant 51: the FP64 tensor-core (DMMA) kernel for even n >= 10.
