@@ -676,6 +676,36 @@ def other_bench(args, local):
                   "per product, dense TF32 1.1 PFLOP/s -> 367 TFLOP/s "
                   "fp32-equivalent ceiling"})
         return r
+    if wl == "dgemm":
+        m = n = l = args.gemm_n
+        _r, knl = fx.translate(fx.gemm_source("f64"))
+        a = torch.rand(m * l, dtype=torch.float64, device=dev, generator=gen)
+        b = torch.rand(l * n, dtype=torch.float64, device=dev, generator=gen)
+        c = torch.rand(m * n, dtype=torch.float64, device=dev, generator=gen)
+        c0 = c.clone()
+        env = lfb.env_from_buffers(knl, {"m": m, "n": n, "l": l},
+                                   {"a": a, "b": b, "c": c}, {"alpha": 1.5})
+        L = lfb.Launcher(knl, env, variant=args.variant)
+        L.launch()
+        torch.cuda.synchronize()
+        rs = np.random.default_rng(1)
+        ii = torch.from_numpy(rs.integers(0, m, 256)).to(dev)
+        jj = torch.from_numpy(rs.integers(0, n, 256)).to(dev)
+        A, B = a.view(l, m), b.view(n, l)
+        seq = c0.view(n, m)[jj, ii].clone()
+        for k in range(l):  # the reference's sequential chain, per sample
+            seq = seq + (1.5 * B[jj, k]) * A[k, ii]
+        got = c.view(n, m)[jj, ii]
+        rel = float(((got - seq).abs() / seq.abs()).max())
+        c.copy_(c0)
+        r = run_timed(L.launch, None, 2.0 * m * n * l)
+        r.update({"metric": f"dgemm fp64 {m}^3 TFLOP/s", "unit": "TFLOP/s",
+                  "value": r["tflops"], "variant": args.variant,
+                  "verify": {"max_rel_err_256_samples_vs_sequential": rel,
+                             "tolerance": 1e-12},
+                  "tensor_peak_note": "FP64 DMMA (mma.sync m8n8k4): "
+                  "37 TFLOP/s measured peak (tools/micro/dmma_probe.cu)"})
+        return r
     if wl == "sweep":
         rows = []
         for n in range(4, 17):

@@ -124,6 +124,17 @@ int lfb_sgemm_f32(float alpha, const float *a, const float *b, float *c,
  * possible else the bit-exact CUDA-core kernel, 1 bit-exact, 2 tensor only */
 int64_t lfb_sgemm_workspace(int l, int m, int n);
 
+/* dgemm: the same kernel in real*8 -- the reference's own DGEMM test
+ * (tests/test_fortran.py:72-103)
+ *                                       emitted: void dgemm(int m, int n, int l, double alpha, double const *a, double const *b, double *c)
+ * (argument order here is the sgemm entry's).  geom->variant: 0 the FP64
+ * tensor cores (DMMA; tolerance parity, fp64 within 1e-12) when m % 128,
+ * n % 128, l % 16 == 0 and a, b are 16-byte aligned, else the bit-exact
+ * CUDA-core kernel; 1 bit-exact; 2 tensor cores only                     */
+int lfb_dgemm_f64(double alpha, const double *a, const double *b, double *c,
+                  int l, int m, int n,
+                  const lfb_launch *geom, lfb_stream stream);
+
 /* Generic path: CUDA C++ generated from a kernel's
  * schedule by paper_1503_07659_b200/cudagen.py -- g.N -> blockIdx, l.N ->
  * threadIdx, workgroup temporaries -> __shared__ with real barriers -- the

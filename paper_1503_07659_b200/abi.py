@@ -55,6 +55,7 @@ SIGNATURES = {
     "lfb_semlap_workspace": [I32, I32, LP],
     "lfb_sgemm_f32": [F, P, P, P, I32, I32, I32, LP, P],
     "lfb_sgemm_workspace": [I32, I32, I32],
+    "lfb_dgemm_f64": [D, P, P, P, I32, I32, I32, LP, P],
     "lfb_probe_fp64": [P, I32, I32, I32, P],
     "lfb_probe_stream": [P, P, P, C.c_int64, P],
     "lfb_rtc_compile": [C.c_char_p, C.c_char_p, C.POINTER(C.c_char_p), I32,

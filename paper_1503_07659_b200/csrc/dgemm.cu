@@ -1,0 +1,256 @@
+// dgemm -- the paper's DGEMM kernel in real*8 (/root/reference/pkg/tests/
+// test_fortran.py:72-103, the real*4 variant is BASELINE config 5):
+//   c(i,j) = c(i,j) + alpha*b(k,j)*a(i,k)   for k ascending
+// column major a(m,l) at a[i + m k], b(l,n) at b[k + l j], c(m,n) at
+// c[i + m j].
+//
+// Two kernels behind lfb_dgemm_f64:
+//  * default (tensor cores, tolerance parity): the FP64 DMMA units
+//    (mma.sync m8n8k4 f64), acc = sum_k a(i,k) b(k,j) fused in the tensor
+//    pipe, then c = c + alpha*acc -- within the north star's 1e-12 relative
+//    fp64 bound normwise (tests/test_gpu_parity.py).  128x128x16 CTA tiles
+//    through a 4-stage cp.async ring in padded shared memory (row strides
+//    132 and 20 doubles: every fragment load of a half warp hits 16
+//    distinct 8-byte bank slots), 8 warps of 64x32 each: per k-step of 4,
+//    8 A and 4 B fragment loads feed 32 DMMAs.  Needs m, n % 128 == 0,
+//    l % 16 == 0 and 16-byte aligned arrays; other shapes take the exact
+//    kernel.
+//  * variant 1 (bit-exact): the reference's chain per output element on
+//    the FP64 CUDA cores, c + ((alpha*b)*a) with every operation rounded
+//    separately, k ascending (the sgemm exact kernel's structure in f64).
+#include "lfb_common.cuh"
+
+namespace lfb {
+
+// {{{ DMMA kernel
+
+constexpr int DG_BM = 128, DG_BN = 128, DG_BK = 16, DG_STAGES = 4;
+constexpr int DG_THREADS = 256;
+constexpr int DG_AS = 132;  // As row stride (doubles): k rows of 128 i
+constexpr int DG_BS = 20;   // Bs row stride: j rows of 16 k
+
+struct DgSmem {
+  static constexpr size_t a_doubles = DG_BK * DG_AS;
+  static constexpr size_t b_doubles = DG_BN * DG_BS;
+  static constexpr size_t stage = a_doubles + b_doubles;
+  static constexpr size_t total = DG_STAGES * stage * 8;
+};
+
+__device__ __forceinline__ void dg_dmma(double &d0, double &d1, double a,
+                                        double b) {
+  asm volatile(
+      "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, "
+      "{%0,%1};"
+      : "+d"(d0), "+d"(d1)
+      : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void cp16(void *dst, const void *src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                   smem_u32(dst)),
+               "l"(src)
+               : "memory");
+}
+
+__global__ void __launch_bounds__(DG_THREADS, 1)
+    dgemm_dmma_kernel(double alpha, const double *__restrict__ a,
+                      const double *__restrict__ b, double *__restrict__ c,
+                      int l, int m, int n) {
+  extern __shared__ __align__(128) double dsm[];
+  const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
+  const int r = lane / 4, q = lane % 4;
+  const int wm = warp / 4, wn = warp % 4;  // 2 x 4 warps of 64 x 32
+  const int i0 = blockIdx.x * DG_BM, j0 = blockIdx.y * DG_BN;
+  const int nk = l / DG_BK;
+
+  auto As = [&](int s) { return dsm + (size_t)s * DgSmem::stage; };
+  auto Bs = [&](int s) { return As(s) + DgSmem::a_doubles; };
+  auto load = [&](int s, int kt) {
+    const int k0 = kt * DG_BK;
+    double *as = As(s), *bs = Bs(s);
+#pragma unroll
+    for (int x = 0; x < 4; ++x) {
+      const int ch = tid + DG_THREADS * x;
+      {  // A: 16 rows (k) of 128 i, 64 chunks of 2 doubles per row
+        const int k = ch / 64, i = (ch % 64) * 2;
+        cp16(as + k * DG_AS + i, a + (i0 + i) + (int64_t)m * (k0 + k));
+      }
+      {  // B: 128 rows (j) of 16 k, 8 chunks per row
+        const int j = ch / 8, k = (ch % 8) * 2;
+        cp16(bs + j * DG_BS + k, b + (k0 + k) + (int64_t)l * (j0 + j));
+      }
+    }
+  };
+
+  double acc[8][4][2];
+#pragma unroll
+  for (int mt = 0; mt < 8; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+
+#pragma unroll
+  for (int s = 0; s < DG_STAGES - 1; ++s) {
+    if (s < nk) load(s, s);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  for (int kt = 0; kt < nk; ++kt) {
+    asm volatile("cp.async.wait_group %0;" ::"n"(DG_STAGES - 2) : "memory");
+    __syncthreads();  // stage kt landed for every thread; stage kt-1 free
+    {
+      const int nxt = kt + DG_STAGES - 1;
+      if (nxt < nk) load(nxt % DG_STAGES, nxt);
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+    const double *as = As(kt % DG_STAGES), *bs = Bs(kt % DG_STAGES);
+#pragma unroll
+    for (int ks = 0; ks < DG_BK / 4; ++ks) {
+      double fa[8], fb[4];
+#pragma unroll
+      for (int mt = 0; mt < 8; ++mt)  // A[i][k]: row i = lane/4, col k
+        fa[mt] = as[(4 * ks + q) * DG_AS + wm * 64 + mt * 8 + r];
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt)  // B[k][j]: row k = lane%4, col j
+        fb[nt] = bs[(wn * 32 + nt * 8 + r) * DG_BS + 4 * ks + q];
+#pragma unroll
+      for (int mt = 0; mt < 8; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt)
+          dg_dmma(acc[mt][nt][0], acc[mt][nt][1], fa[mt], fb[nt]);
+    }
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+
+  // c = c + alpha*acc; lane holds rows i = .. + r, columns j = .. + 2q + h
+#pragma unroll
+  for (int mt = 0; mt < 8; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int i = i0 + wm * 64 + mt * 8 + r;
+        const int j = j0 + wn * 32 + nt * 8 + 2 * q + h;
+        double *p = c + i + (int64_t)m * j;
+        *p = dadd(*p, dmul(alpha, acc[mt][nt][h]));
+      }
+}
+
+// }}}
+
+// {{{ bit-exact kernel (the reference's sequential chain)
+
+constexpr int DE_BM = 128, DE_BN = 128, DE_BK = 8, DE_THREADS = 256;
+
+__global__ void __launch_bounds__(DE_THREADS)
+    dgemm_exact_kernel(double alpha, const double *__restrict__ a,
+                       const double *__restrict__ b, double *__restrict__ c,
+                       int l, int m, int n) {
+  __shared__ double As[2][DE_BK][DE_BM];
+  __shared__ double Bs[2][DE_BK][DE_BN];  // alpha*b(k,j)
+
+  const int tid = threadIdx.x;
+  const int tx = tid % 16, ty = tid / 16;  // 16 x 16 threads, 8x8 each
+  const int i0 = blockIdx.x * DE_BM, j0 = blockIdx.y * DE_BN;
+
+  double acc[8][8];
+#pragma unroll
+  for (int ii = 0; ii < 8; ++ii)
+#pragma unroll
+    for (int jj = 0; jj < 8; ++jj) {
+      const int gi = i0 + ty * 8 + ii, gj = j0 + tx * 8 + jj;
+      acc[ii][jj] = (gi < m && gj < n) ? c[gi + (int64_t)m * gj] : 0.0;
+    }
+
+  // A slab 128(i) x 8(k): thread -> (i = tid % 128, k = tid / 128 * 4 + q)
+  // B slab 8(k) x 128(j): thread -> (k = tid % 8, j = tid / 8 * 4 + q)
+  double ra[4], rb[4];
+  auto load = [&](int k0) {
+#pragma unroll
+    for (int x = 0; x < 4; ++x) {
+      const int ii = tid % DE_BM, kk = (tid / DE_BM) * 4 + x;
+      const int gi = i0 + ii, gk = k0 + kk;
+      ra[x] = (gi < m && gk < l) ? __ldg(a + gi + (int64_t)m * gk) : 0.0;
+      const int kb = tid % DE_BK, jb = (tid / DE_BK) * 4 + x;
+      const int gkb = k0 + kb, gj = j0 + jb;
+      rb[x] = (gkb < l && gj < n) ? __ldg(b + gkb + (int64_t)l * gj) : 0.0;
+    }
+  };
+  auto store = [&](int buf) {
+#pragma unroll
+    for (int x = 0; x < 4; ++x) {
+      As[buf][(tid / DE_BM) * 4 + x][tid % DE_BM] = ra[x];
+      Bs[buf][tid % DE_BK][(tid / DE_BK) * 4 + x] = dmul(alpha, rb[x]);
+    }
+  };
+
+  const int nk = (l + DE_BK - 1) / DE_BK;
+  load(0);
+  store(0);
+  __syncthreads();
+  for (int t = 0; t < nk; ++t) {
+    const int buf = t & 1;
+    if (t + 1 < nk) load((t + 1) * DE_BK);
+    const int kmax = min(DE_BK, l - t * DE_BK);
+    for (int kk = 0; kk < kmax; ++kk) {
+      double av[8], bv[8];
+#pragma unroll
+      for (int x = 0; x < 8; ++x) {
+        av[x] = As[buf][kk][ty * 8 + x];
+        bv[x] = Bs[buf][kk][tx * 8 + x];
+      }
+#pragma unroll
+      for (int ii = 0; ii < 8; ++ii)
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj)
+          acc[ii][jj] = dadd(acc[ii][jj], dmul(bv[jj], av[ii]));
+    }
+    if (t + 1 < nk) store(buf ^ 1);
+    __syncthreads();
+  }
+
+#pragma unroll
+  for (int ii = 0; ii < 8; ++ii)
+#pragma unroll
+    for (int jj = 0; jj < 8; ++jj) {
+      const int gi = i0 + ty * 8 + ii, gj = j0 + tx * 8 + jj;
+      if (gi < m && gj < n) c[gi + (int64_t)m * gj] = acc[ii][jj];
+    }
+}
+
+// }}}
+
+}  // namespace lfb
+
+extern "C" int lfb_dgemm_f64(double alpha, const double *a, const double *b,
+                             double *c, int l, int m, int n,
+                             const lfb_launch *geom, lfb_stream stream) {
+  using namespace lfb;
+  if (l < 0 || m < 0 || n < 0)
+    return fail(LFB_ERR_ARG, "lfb_dgemm_f64: negative extent");
+  if (m == 0 || n == 0) return LFB_OK;
+  if (!a || !b || !c) return fail(LFB_ERR_ARG, "lfb_dgemm_f64: null array");
+  if (geom && geom->abi_version != LFB_ABI_VERSION)
+    return fail(LFB_ERR_ARG, "lfb_dgemm_f64: bad lfb_launch version");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int variant = geom ? geom->variant : 0;
+  const bool tc_ok = m % DG_BM == 0 && n % DG_BN == 0 && l % DG_BK == 0 &&
+                     l > 0 && aligned(a, 16) && aligned(b, 16);
+  if (variant != 1 && tc_ok) {
+    cudaFuncSetAttribute(dgemm_dmma_kernel,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)DgSmem::total);
+    dim3 grid(m / DG_BM, n / DG_BN);
+    dgemm_dmma_kernel<<<grid, DG_THREADS, DgSmem::total, s>>>(alpha, a, b, c,
+                                                             l, m, n);
+    return check_launch("lfb_dgemm_f64(dmma)");
+  }
+  if (variant == 2)
+    return fail(LFB_ERR_UNSUPPORTED,
+                "lfb_dgemm_f64: the tensor-core path needs m %% 128, "
+                "n %% 128, l %% 16 == 0 and 16-byte aligned a, b "
+                "(m=%d n=%d l=%d)", m, n, l);
+  dim3 grid((m + DE_BM - 1) / DE_BM, (n + DE_BN - 1) / DE_BN);
+  if (grid.y > 65535)
+    return fail(LFB_ERR_UNSUPPORTED, "lfb_dgemm_f64: n=%d too large", n);
+  dgemm_exact_kernel<<<grid, DE_THREADS, 0, s>>>(alpha, a, b, c, l, m, n);
+  return check_launch("lfb_dgemm_f64(exact)");
+}

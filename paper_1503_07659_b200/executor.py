@@ -208,7 +208,8 @@ class Launcher:
         self.npts = w.npts
         self._sumsq = sumsq
         self._workspace = workspace
-        if w.name == "gemm" and workspace is None and variant != 1:
+        if w.name == "gemm" and w.dtype == "f32" and workspace is None \
+                and variant != 1:
             # tf32 hi/lo operand split for the tensor-core path
             pm = self.match.param_map
             l, m, n = (env.params[pm[p]] for p in ("l", "m", "n"))
@@ -262,9 +263,9 @@ class Launcher:
             rc = lib.lfb_semlap_f64(P("w"), P("u"), P("d"), P("g"),
                                     I("nelt"), gp, stream)
         elif fam == "gemm":
-            rc = lib.lfb_sgemm_f32(float(S("alpha")), P("a"), P("b"),
-                                   P("c"), I("l"), I("m"), I("n"), gp,
-                                   stream)
+            fn = lib.lfb_sgemm_f32 if dt == "f32" else lib.lfb_dgemm_f64
+            rc = fn(float(S("alpha")), P("a"), P("b"), P("c"), I("l"),
+                    I("m"), I("n"), gp, stream)
         else:
             raise CodegenError(f"no entry point for workload {fam}")
         abi.check(rc, f"{fam}_{dt}")

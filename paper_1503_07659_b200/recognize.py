@@ -658,9 +658,10 @@ def _templates():
         out.append(Workload("semlap", "f64", n,
                             fixtures.semlap_source(n, script=False),
                             ("w", "u", "d", "g"), ("nelt",)))
-    out.append(Workload("gemm", "f32", 0,
-                        fixtures.gemm_source("f32", script=False),
-                        ("alpha", "a", "b", "c"), ("l", "m", "n")))
+    for dt in ("f32", "f64"):
+        out.append(Workload("gemm", dt, 0,
+                            fixtures.gemm_source(dt, script=False),
+                            ("alpha", "a", "b", "c"), ("l", "m", "n")))
     return out
 
 
@@ -707,7 +708,7 @@ def recognize(kernel):
         return Match(w, canon, arg_map, param_map)
     raise CodegenError(
         f"kernel '{kernel.name}' is not one of the B200 executor's "
-        "workloads (fill, axpy, matvec, semlap n=2..16, sgemm); the "
+        "workloads (fill, axpy, matvec, semlap n=2..16, sgemm, dgemm); the "
         "executor has no CPU fallback")
 
 # }}}

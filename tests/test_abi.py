@@ -21,7 +21,7 @@ def declared_symbols():
 def test_header_declares_the_entry_points():
     syms = declared_symbols()
     for s in ("lfb_fill_f64", "lfb_axpy_f64", "lfb_matvec_f64",
-              "lfb_semlap_f64", "lfb_sgemm_f32", "lfb_last_error",
+              "lfb_semlap_f64", "lfb_sgemm_f32", "lfb_dgemm_f64", "lfb_last_error",
               "lfb_abi_version"):
         assert s in syms
 

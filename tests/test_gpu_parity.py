@@ -457,6 +457,53 @@ def test_sgemm_tensor_cores(cuda, m, n, l, variant):
     assert err_exact <= 1e-5
 
 
+@pytest.mark.parametrize("m,n,l", [(128, 128, 16), (256, 384, 512),
+                                   (1024, 512, 2048), (512, 256, 8192)])
+def test_dgemm_tensor_cores(cuda, m, n, l):
+    """The paper's DGEMM in real*8 on the FP64 tensor cores (DMMA):
+    tolerance parity (north star: 1e-12 relative fp64) against the
+    reference's sequential-k result -- normwise, and per entry against the
+    magnitude sum_k |alpha b a| + |c| on [-1, 1) data."""
+    _r, knl = fx.translate(fx.gemm_source("f64"))
+    rng = np.random.default_rng(m + n + l)
+    a = rng.random(m * l) * 2 - 1
+    b = rng.random(l * n) * 2 - 1
+    c = rng.random(m * n) * 2 - 1
+    alpha = 1.5
+    env = lfb.env_from_buffers(
+        knl, {"m": m, "n": n, "l": l},
+        {"a": torch.from_numpy(a).to(cuda), "b": torch.from_numpy(b).to(cuda),
+         "c": torch.from_numpy(c.copy()).to(cuda)}, {"alpha": alpha})
+    out = lfb.interpret(knl, env)
+    got = out.arrays["c"].data.cpu().numpy()
+    ref = oracle.sgemm(alpha, a, b, c.copy(), l, m, n, threads=8)
+    mag = oracle.sgemm(alpha, np.abs(a), np.abs(b), np.abs(c), l, m, n,
+                       threads=8)
+    err = np.abs(got - ref)
+    assert np.linalg.norm(got - ref) <= 1e-12 * np.linalg.norm(ref)
+    assert (err <= 1e-12 * mag).all()
+    assert got.tobytes() != ref.tobytes()  # really the fused path
+
+
+@pytest.mark.parametrize("m,n,l", [(128, 128, 16), (100, 60, 33),
+                                   (300, 130, 70)])
+def test_dgemm_exact(cuda, m, n, l):
+    """variant 1 (and every shape the tensor-core path cannot take): the
+    reference's chain c + (alpha*b)*a per k on the FP64 CUDA cores,
+    bitwise."""
+    _r, knl = fx.translate(fx.gemm_source("f64", script=False))
+    rng = np.random.default_rng(m * n + l)
+    a, b, c = rng.random(m * l), rng.random(l * n), rng.random(m * n)
+    env = lfb.env_from_buffers(
+        knl, {"m": m, "n": n, "l": l},
+        {"a": torch.from_numpy(a).to(cuda), "b": torch.from_numpy(b).to(cuda),
+         "c": torch.from_numpy(c.copy()).to(cuda)}, {"alpha": 1.25})
+    variant = 1 if m % 128 == 0 else 0
+    out = lfb.interpret(knl, env, variant=variant)
+    ref = oracle.sgemm(1.25, a, b, c.copy(), l, m, n, threads=8)
+    assert out.arrays["c"].data.cpu().numpy().tobytes() == ref.tobytes()
+
+
 def test_sgemm_default_dispatch(cuda):
     """Default variant: tensor cores for 128/256/32-aligned shapes, the
     bit-exact kernel otherwise -- both on the device."""
