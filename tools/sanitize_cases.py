@@ -1,0 +1,99 @@
+"""Small launches of every hand-written kernel family, for
+compute-sanitizer (memcheck / racecheck / synccheck): tools/gpu_sanitize.sh.
+Each case also checks its result against the oracle so a sanitizer run is a
+parity run too."""
+import os
+import sys
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, REPO)
+sys.path.insert(0, os.path.join(REPO, "oracle"))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import oracle  # noqa: E402
+import paper_1503_07659_b200 as lfb  # noqa: E402
+from paper_1503_07659_b200 import fixtures as fx  # noqa: E402
+
+dev = torch.device("cuda", 0)
+
+
+def sem(n, nelt, variant, exact=True):
+    _r, knl = fx.translate(fx.semlap_source(n, block=1))
+    g = torch.Generator(device=dev).manual_seed(n)
+    u = torch.rand(nelt * n ** 3, dtype=torch.float64, device=dev,
+                   generator=g) * 2 - 1
+    gg = torch.rand(6 * nelt * n ** 3, dtype=torch.float64, device=dev,
+                    generator=g)
+    d = torch.rand(n * n, dtype=torch.float64, device=dev, generator=g)
+    w = torch.zeros_like(u)
+    env = lfb.env_from_buffers(knl, {"nelt": nelt},
+                               {"u": u, "d": d, "g": gg, "w": w})
+    lfb.Launcher(knl, env, variant=variant).launch()
+    torch.cuda.synchronize()
+    ref = oracle.semlap(np.zeros(u.numel()), u.cpu().numpy(), d.cpu().numpy(),
+                        gg.cpu().numpy(), n, nelt)
+    got = w.cpu().numpy()
+    ok = got.tobytes() == ref.tobytes() if exact else \
+        np.abs(got - ref).max() <= 1e-12 * np.abs(ref).max()
+    print(f"semlap n={n} nelt={nelt} variant={variant}: "
+          f"{'ok' if ok else 'MISMATCH'}", flush=True)
+    return ok
+
+
+def gemm(dt, m, n, l, variant, exact):
+    _r, knl = fx.translate(fx.gemm_source(dt))
+    npt = np.float32 if dt == "f32" else np.float64
+    rng = np.random.default_rng(1)
+    a, b, c = (rng.random(s).astype(npt) for s in (m * l, l * n, m * n))
+    env = lfb.env_from_buffers(
+        knl, {"m": m, "n": n, "l": l},
+        {"a": torch.from_numpy(a).to(dev), "b": torch.from_numpy(b).to(dev),
+         "c": torch.from_numpy(c.copy()).to(dev)}, {"alpha": 1.5})
+    out = lfb.interpret(knl, env, variant=variant)
+    got = out.arrays["c"].data.cpu().numpy()
+    ref = oracle.sgemm(npt(1.5), a, b, c.copy(), l, m, n, threads=8)
+    tol = 1e-5 if dt == "f32" else 1e-12
+    ok = got.tobytes() == ref.tobytes() if exact else \
+        np.linalg.norm(got - ref) <= tol * np.linalg.norm(ref)
+    print(f"{dt}gemm {m}x{n}x{l} variant={variant}: "
+          f"{'ok' if ok else 'MISMATCH'}", flush=True)
+    return ok
+
+
+def streams():
+    n = 100003
+    _r, kf = fx.translate(fx.fill_source("f64"))
+    env = lfb.make_device_env(kf, {"n": n}, {"a": 0.5}, device=dev)
+    ok = bool((lfb.interpret(kf, env).arrays["out"].data == 0.5).all())
+    _r, km = fx.translate(fx.matvec_source("f64"))
+    nn = 512
+    a = torch.rand(nn * nn, dtype=torch.float64, device=dev)
+    x = torch.rand(nn, dtype=torch.float64, device=dev)
+    for v in (0, 3):
+        y = torch.zeros(nn, dtype=torch.float64, device=dev)
+        env = lfb.env_from_buffers(km, {"n": nn}, {"a": a, "x": x, "y": y})
+        lfb.interpret(km, env, inplace=True, variant=v)
+        ref = oracle.matvec(np.zeros(nn), a.cpu().numpy(), x.cpu().numpy(),
+                            nn)
+        ok &= float(np.abs(y.cpu().numpy() - ref).max()) <= 1e-12 * nn
+    print(f"fill/matvec: {'ok' if ok else 'MISMATCH'}", flush=True)
+    return ok
+
+
+if __name__ == "__main__":
+    which = sys.argv[1] if len(sys.argv) > 1 else "all"
+    oks = []
+    if which in ("all", "sem"):
+        oks += [sem(8, 37, 0), sem(8, 37, 50, False), sem(8, 37, 39),
+                sem(4, 33, 0), sem(7, 9, 61, False), sem(9, 5, 0),
+                sem(12, 5, 0), sem(15, 3, 51, False), sem(16, 3, 51, False)]
+    if which in ("all", "gemm"):
+        oks += [gemm("f32", 256, 256, 64, 0, False),
+                gemm("f32", 100, 60, 33, 1, True),
+                gemm("f64", 256, 128, 64, 0, False),
+                gemm("f64", 100, 60, 33, 1, True)]
+    if which in ("all", "stream"):
+        oks.append(streams())
+    sys.exit(0 if all(oks) else 1)
