@@ -706,6 +706,44 @@ def other_bench(args, local):
                   "tensor_peak_note": "FP64 DMMA (mma.sync m8n8k4): "
                   "37 TFLOP/s measured peak (tools/micro/dmma_probe.cu)"})
         return r
+    if wl == "generic":
+        # the generic engine (CUDA generated from the schedule, NVRTC) on
+        # BASELINE workloads the hand-written kernels also cover: what a
+        # kernel outside the recognised set can expect
+        from paper_1503_07659_b200.generic import GenericLauncher
+        rows = {}
+        n = 1 << 24
+        _r, kf = fx.translate(fx.fill_source("f64"))
+        outs = [torch.empty(n, dtype=torch.float64, device=dev)
+                for _ in range(4)]
+        envs = [lfb.env_from_buffers(kf, {"n": n}, {"out": o}, {"a": 1.5})
+                for o in outs]
+        r = run_rotating([GenericLauncher(kf, e).launch for e in envs], 8 * n)
+        rows["fill_f64_2^24"] = {"GB/s": r["roofline"]["achieved"],
+                                 "frac": r["roofline"]["frac"]}
+        _r, ka = fx.translate(fx.axpy_source("f64"))
+        envs = []
+        for _ in range(3):
+            x = torch.rand(n, dtype=torch.float64, device=dev, generator=gen)
+            y = torch.rand(n, dtype=torch.float64, device=dev, generator=gen)
+            envs.append(lfb.env_from_buffers(ka, {"n": n}, {"y": y, "x": x},
+                                             {"alpha": 1.25}))
+        r = run_rotating([GenericLauncher(ka, e).launch for e in envs],
+                         24 * n)
+        rows["axpy_f64_2^24"] = {"GB/s": r["roofline"]["achieved"],
+                                 "frac": r["roofline"]["frac"]}
+        m = nn = l = 2048
+        _r, kg = fx.translate(fx.gemm_source("f64"))
+        a = torch.rand(m * l, dtype=torch.float64, device=dev, generator=gen)
+        b = torch.rand(l * nn, dtype=torch.float64, device=dev, generator=gen)
+        c = torch.rand(m * nn, dtype=torch.float64, device=dev, generator=gen)
+        env = lfb.env_from_buffers(kg, {"m": m, "n": nn, "l": l},
+                                   {"a": a, "b": b, "c": c}, {"alpha": 1.5})
+        r = run_timed(GenericLauncher(kg, env).launch, None, 2.0 * m * nn * l)
+        rows["dgemm_paper_script_2048^3"] = {"TFLOP/s": r["tflops"],
+                                             "ms": r["ms_per_step"]}
+        return {"metric": "generic engine (generated CUDA) GB/s | TFLOP/s",
+                "rows": rows, "engine": "generic (cudagen.py, NVRTC sm_100a)"}
     if wl == "sweep":
         rows = []
         for n in range(4, 17):

@@ -10,8 +10,10 @@ kernels the hand-written sm_100a kernels (recognize.py) do not cover:
   (codegen.py:89-234); loop bounds from ``loop_bounds`` (241-248) rendered
   with 64-bit integers and floor division;
 * tag -> hardware index exactly as ``emit_opencl_prologue`` (580-588):
-  ``g.N`` -> ``blockIdx``, ``l.N`` -> ``threadIdx``; the residual guard of
-  ``opencl_guard`` (590-612, restated in launch.py);
+  ``g.N`` -> the work-group index, ``l.N`` -> ``threadIdx``; the residual
+  guard of ``opencl_guard`` (590-612, restated in launch.py).  Work-groups
+  are walked by persistent CTAs (grid-stride over the logical g.0 x g.1 x
+  g.2 space) so small work-groups are not CTA-launch bound;
 * workgroup temporaries (``precompute`` with an ``l.*`` sweep iname,
   transforms.py:597-599) -> ``__shared__`` arrays with real
   ``__syncthreads()`` around the loop nests that write them.  A fetch nest
@@ -670,12 +672,15 @@ class _Emitter:
                 decl.append(f"{q}{ct} {name}[{size}];")
 
         pro = []
+        gnames = {}   # g axis -> iname
         block = [1, 1, 1]
         for iname in self.parallel:
             kind, axis = k.iname_tags[iname].split(".")
             comp = "xyz"[int(axis)]
-            src = "blockIdx" if kind == "g" else "threadIdx"
-            pro.append(f"const i64 {iname} = (i64){src}.{comp};")
+            if kind == "g":
+                gnames[int(axis)] = iname
+                continue
+            pro.append(f"const i64 {iname} = (i64)threadIdx.{comp};")
             if kind == "l":
                 _lo, ups = codegen.loop_bounds(k, iname, [])
                 if not all(b.is_plain_affine() and b.as_affine().is_constant()
@@ -689,8 +694,24 @@ class _Emitter:
         pro.append("const i64 lfb_nthreads = (i64)blockDim.x * blockDim.y * "
                    "blockDim.z;")
 
+        # work-groups in a grid-stride loop over a capped 1-D grid: the
+        # logical g.0 x g.1 x g.2 space (extents lfb_G0..2) is walked by
+        # persistent CTAs, so tiny work-groups do not leave the GPU
+        # CTA-launch bound; barriers stay uniform (every thread of a CTA
+        # walks the same groups), shared tiles get a barrier between groups
         self.lines = []
         self.ind = 1
+        self.line("const i64 lfb_ng = lfb_G0 * lfb_G1 * lfb_G2;")
+        self.line("for (i64 lfb_g = (i64)blockIdx.x; lfb_g < lfb_ng; "
+                  "lfb_g += (i64)gridDim.x) {")
+        self.ind += 1
+        for axis, iname in sorted(gnames.items()):
+            div = " * ".join(f"lfb_G{a}" for a in range(axis)) or "1"
+            self.line(f"const i64 {iname} = (lfb_g / ({div})) % lfb_G{axis};")
+        for name in sorted(k.temporaries):
+            t = k.temporaries[name]
+            if not t.shape:
+                self.line(f"{name} = 0;")
         if shared and guard_text:
             self.line(f"const bool lfb_in = {guard_text};")
             self.walk(self.tree, {"wg": shared, "guard": "stmt"})
@@ -702,6 +723,10 @@ class _Emitter:
             self.line("}")
         else:
             self.walk(self.tree, {"wg": shared, "guard": None})
+        if shared:
+            self.line("__syncthreads();  // tiles free for the next group")
+        self.ind -= 1
+        self.line("}")
         body = self.lines
 
         params = tuple(sorted(k.param_names))
@@ -719,6 +744,9 @@ class _Emitter:
             if p not in argnames:
                 sig.append(f"i64 {p}")
                 order.append(p)
+        for a in range(3):  # logical work-group extents (launch geometry)
+            sig.append(f"i64 lfb_G{a}")
+            order.append(f"lfb_G{a}")
         nthreads = block[0] * block[1] * block[2]
         if nthreads > 1024:
             raise CodegenError(

@@ -74,6 +74,16 @@ def _module(prog, device_index):
 _CTY = {"f64": C.c_double, "f32": C.c_float, "i32": C.c_int32}
 
 
+_SMS = {}
+
+
+def _sm_count(index):
+    if index not in _SMS:
+        _SMS[index] = torch.cuda.get_device_properties(index) \
+            .multi_processor_count
+    return _SMS[index]
+
+
 class GenericLauncher:
     """Prepared launch of the generated kernel (same interface as
     executor.Launcher)."""
@@ -95,9 +105,13 @@ class GenericLauncher:
                 stream = torch.cuda.current_stream(dev).cuda_stream
         vals = []
         args = {a.name: a for a in self.kernel.args}
+        geo = self.geometry
+        gext = [max(1, int(x)) for x in geo.group_extent]
         for name in prog.arg_order:
             a = args.get(name)
-            if a is None:                      # a parameter (int64)
+            if name.startswith("lfb_G"):       # logical work-group extents
+                vals.append(C.c_int64(gext[int(name[5:])]))
+            elif a is None:                    # a parameter (int64)
                 vals.append(C.c_int64(int(env.params[name])))
             elif a.kind == "global-array":
                 vals.append(C.c_void_p(env.arrays[name].data.data_ptr()))
@@ -105,8 +119,12 @@ class GenericLauncher:
                 vals.append(_CTY[a.dtype](env.scalars[name]))
         argv = (C.c_void_p * len(vals))(
             *[C.cast(C.pointer(v), C.c_void_p) for v in vals])
-        geo = self.geometry
-        grid = (C.c_int64 * 3)(*geo.group_extent)
+        nthreads = prog.block[0] * prog.block[1] * prog.block[2]
+        ngroups = gext[0] * gext[1] * gext[2]
+        idx = dev.index if dev.index is not None \
+            else torch.cuda.current_device()
+        cap = _sm_count(idx) * max(1, 2048 // max(32, nthreads))
+        grid = (C.c_int64 * 3)(min(ngroups, cap), 1, 1)
         block = (C.c_int32 * 3)(*prog.block)
         abi.check(abi.load().lfb_module_launch(mod, grid, block, 0, argv,
                                                stream),
