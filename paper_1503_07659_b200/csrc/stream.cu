@@ -204,7 +204,10 @@ static int fill_impl(const char *what, T *out, T a, int n,
       if (sms <= 0) sms = 148;
       const int64_t nbytes = nvec * 16;
       const int64_t chunks = (nbytes + FILL_CHUNK - 1) / FILL_CHUNK;
-      const int grid = (int)(chunks < sms ? chunks : sms);
+      const int per_sm = (geom && geom->ctas_per_sm > 0) ? geom->ctas_per_sm
+                                                          : 1;
+      const int64_t cap = (int64_t)sms * per_sm;
+      const int grid = (int)(chunks < cap ? chunks : cap);
       cudaFuncSetAttribute(fill_bulk_kernel<T>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize,
                            FILL_CHUNK);
