@@ -28,9 +28,12 @@
  *     buffers.  Scratch (the SEM norm partials) is caller provided.
  *   - Index arithmetic inside kernels is 64-bit (the emitted C uses int and
  *     overflows past 2^31 elements, SURVEY.md §7 hard part 2).
- *   - Results are bitwise identical to the reference's execution of the same
- *     kernel (fill, axpy, matvec, semlap); sgemm is within the fp32 tolerance
- *     documented in DESIGN.md.
+ *   - geom->variant 0 results are bitwise identical to the reference's
+ *     execution of the same kernel for fill, axpy and semlap; matvec's
+ *     default (split-j) and semlap variants 50/51/61 (fused multiply-adds)
+ *     are within the north star's fp64 bound (1e-12 relative), matvec
+ *     variants 1/3 bitwise; sgemm / dgemm tensor-core paths are within the
+ *     fp32 / fp64 tolerances, their variant 1 bitwise.
  */
 #ifndef LOOPFORGE_B200_H
 #define LOOPFORGE_B200_H
@@ -96,7 +99,10 @@ int lfb_axpy_f32(float *y, const float *x, float alpha, int n,
 
 /* matvec: y[i] = sum_j a[i + n*j]*x[j], sequential j, s starts at 0
  *                                       emitted: void matvec(double *y, double const *a, double const *x, int n)
- * reference: SURVEY.md Appendix B (extract_subst + precompute on x)       */
+ * reference: SURVEY.md Appendix B (extract_subst + precompute on x)
+ * geom->variant: 0 split-j (4 column parts summed in order; fp64 within
+ * 1e-12) when n >= 256, 1 bitwise direct loads, 2 split-j only, 3 bitwise
+ * TMA kernel                                                              */
 int lfb_matvec_f64(double *y, const double *a, const double *x, int n,
                    const lfb_launch *geom, lfb_stream stream);
 
@@ -104,7 +110,11 @@ int lfb_matvec_f64(double *y, const double *a, const double *x, int n,
  *                                       emitted: void semlap(double *w, double const *u, double const *d, double const *g, int nelt)
  * reference: SURVEY.md Appendix A; layouts u,w (n,n,n,nelt) strides
  * (1,n,n^2,n^3), d (n,n) strides (1,n), g (6,n,n,n,nelt) strides
- * (1,6,6n,6n^2,6n^3) -- fortran.py:638-658 column-major lowering.        */
+ * (1,6,6n,6n^2,6n^3) -- fortran.py:638-658 column-major lowering.
+ * geom->variant: 0 bitwise (the tuned kernel per order), 50 DFMA mode
+ * (fp64 within 1e-12 per point), 51 FP64 tensor cores (DMMA, n = 9..16),
+ * 60 / 61 two columns per thread (bitwise / DFMA, n = 7, 9..12), other
+ * numbers: tuning alternatives (tests/test_gpu_parity.py)               */
 int lfb_semlap_f64(double *w, const double *u, const double *d,
                    const double *g, int nelt,
                    const lfb_launch *geom, lfb_stream stream);
