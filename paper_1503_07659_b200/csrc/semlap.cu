@@ -615,12 +615,12 @@ static int sem_dispatch(double *w, const double *u, const double *d,
                                      nelt, geom, s, grid_out);
     if (rc != -1) return rc;
   }
-  if (var0 == 51 || (var0 == 50 && n >= 15)) {
-    // FP64 tensor cores (semlap_tc.cu), n = 9..16; the DFMA-mode default
-    // at n = 15, 16, where it beats the column kernels (n = 15: 49 % vs
-    // 38 % of HBM)
-    const int rc = sem_tc_dispatch(n, 51, w, u, d, g, nelt, geom, s,
-                                   grid_out);
+  if ((var0 >= 51 && var0 <= 53) || (var0 == 50 && n >= 12)) {
+    // FP64 tensor cores (semlap_tc.cu), n = 9..16; the interleaved-phase
+    // kernel (52) is the DFMA-mode default for n >= 12, where it beats the
+    // column kernels by 12-28 %
+    const int rc = sem_tc_dispatch(n, var0 == 50 ? 52 : var0, w, u, d, g,
+                                   nelt, geom, s, grid_out);
     if (rc != -1) return rc;
   }
   const int var = var0;

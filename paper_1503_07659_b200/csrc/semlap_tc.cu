@@ -330,6 +330,288 @@ __global__ void __launch_bounds__(G *TcCfg<N>::T, 1)
   if constexpr (SUMSQ) block_sumsq_partial(acc_sq, partials);
 }
 
+// {{{ interleaved-phase DMMA kernel (variant 52)
+//
+// The first DMMA kernel keeps wr / ws of a whole element (2 x 40 KB at
+// n = 16) because phase 2 starts only when phase 1 is complete -- the
+// D-contraction of wt over l needs every slice.  That leaves one 4-warp
+// group per SM, latency bound.  Here the two DMMA sums of phase 2 for slice
+// k (d^T.wr and ws.d) are formed right after phase 1 has produced wr / ws of
+// slice k -- they only need that slice -- and kept per thread (2 values per
+// k); the own-column sum over wt is added once phase 1 is complete.  wr / ws
+// shrink to a 2-slice ring, the ur / us fragments are read straight from the
+// staged u (zeroed smem makes every padded read finite), and 2-3 groups
+// (8-12 warps) fit per SM.  Arithmetic as variant 51 (DFMA mode, within
+// 1e-12; the phase-2 sums are added in a different order).
+template <int N, int G, int SGS, int KS>
+struct Tc2Smem {
+  using C = TcCfg<N>;
+  static constexpr int UST = (C::NP + 2 + 1) / 2 * 2;  // + 8-byte lead
+  static constexpr size_t grp_doubles =
+      (size_t)UST + (size_t)SGS * KS * C::SLAB + 4 * (size_t)C::SL;
+  static constexpr size_t grp_bytes = (grp_doubles * 8 + 127) / 128 * 128;
+  static constexpr size_t bars = 256;
+  static constexpr size_t total = bars + G * grp_bytes;
+};
+
+template <int N, int G, int SGS, int KS, bool SUMSQ>
+__global__ void __launch_bounds__(G *TcCfg<N>::T, 1)
+    semlap_tc2_kernel(double *__restrict__ w, const double *__restrict__ u,
+                      const double *__restrict__ g, int64_t nelt,
+                      double *__restrict__ partials) {
+  using C = TcCfg<N>;
+  using L = Tc2Smem<N, G, SGS, KS>;
+  constexpr int NP = C::NP, T = C::T, KT = C::KT, P = C::P, SL = C::SL;
+  constexpr int N2 = N * N;
+  static_assert(N > 8 && N <= 16, "n = 9..16");
+  static_assert(N % KS == 0, "KS divides n");
+  static_assert(G * (1 + SGS) <= 32, "mbarriers");
+
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t *bars = reinterpret_cast<uint64_t *>(smem);
+
+  const int tid = threadIdx.x;
+  const int grp = tid / T;
+  const int lt = tid % T;
+  const int warp = lt / 32, lane = lt % 32;
+  const int it = warp / C::NT, jt = warp % C::NT;
+  const int r = lane / 4, q = lane % 4;
+  const int j = 8 * jt + r;          // accumulator row
+  const int i0 = 8 * it + 2 * q;     // accumulator columns i0, i0 + 1
+  const bool vj = j < N;
+  const bool v0 = vj && i0 < N, v1 = vj && i0 + 1 < N;
+
+  double *gb = reinterpret_cast<double *>(smem + L::bars +
+                                          (size_t)grp * L::grp_bytes);
+  double *ust0 = gb;                          // u of the element (+ lead)
+  double *slabs = ust0 + L::UST;              // SGS x KS x 6 N^2
+  double *wrr = slabs + SGS * KS * C::SLAB;   // wr: 2 padded slices
+  double *wsr = wrr + 2 * SL;                 // ws: 2 padded slices
+  uint64_t *ubar = bars + grp * (1 + SGS);
+  uint64_t *gbar = ubar + 1;
+
+  const int64_t q0 = (int64_t)blockIdx.x * G + grp;
+  const int64_t Q = (int64_t)gridDim.x * G;
+  const int64_t mine = nelt > q0 ? (nelt - q0 + Q - 1) / Q : 0;
+  auto elem = [&](int64_t m) -> int64_t { return q0 + m * Q; };
+
+  if (tid == 0) {
+    for (int x = 0; x < G * (1 + SGS); ++x) mbar_init(&bars[x], 1);
+    fence_mbar_init();
+  }
+  // zero all group smem once: padded / out-of-element fragment reads are
+  // then finite (they meet zero d entries or feed unstored rows)
+  for (int x = lt; x < (int)(L::grp_bytes / 8); x += T) gb[x] = 0.0;
+  __syncthreads();
+
+  const uint64_t pol = policy_evict_first();
+  const int64_t u_bytes_total = nelt * NP * 8;
+  auto u_lead = [&](int64_t e) -> int { return (int)((e * NP) & 1); };
+  auto u_span = [&](int64_t e) -> int64_t {
+    return ((int64_t)(u_lead(e) + NP) * 8 + 15) / 16 * 16;
+  };
+  auto u_bulk_ok = [&](int64_t e) -> bool {
+    return (e * NP - u_lead(e)) * 8 + u_span(e) <= u_bytes_total;
+  };
+  auto issue_u = [&](int64_t m) {
+    const int64_t e = elem(m);
+    if (u_bulk_ok(e)) {
+      mbar_arrive_expect_tx(ubar, (uint32_t)u_span(e));
+      bulk_g2s_stream(ust0, u + e * NP - u_lead(e), (uint32_t)u_span(e),
+                      ubar, pol);
+    } else {
+      mbar_arrive_expect_tx(ubar, 0);
+    }
+  };
+  auto issue_slab = [&](int64_t sq) {
+    const int64_t e = elem(sq / (N / KS));
+    const int k0 = (int)(sq % (N / KS)) * KS;
+    const int slot = (int)(sq % SGS);
+    mbar_arrive_expect_tx(&gbar[slot], (uint32_t)(KS * C::SLAB * 8));
+    bulk_g2s_stream(slabs + (size_t)slot * KS * C::SLAB,
+                    g + e * 6 * NP + (int64_t)k0 * 6 * N2, KS * C::SLAB * 8,
+                    &gbar[slot], pol);
+  };
+  const int64_t nslabs = mine * (N / KS);
+  if (lt == 0) {
+    if (mine > 0) issue_u(0);
+    for (int64_t x = 0; x < SGS && x < nslabs; ++x) issue_slab(x);
+  }
+
+  double fa_r[KT], fb_s[KT], fa_t[KT], fb_t[KT];
+#pragma unroll
+  for (int ks = 0; ks < KT; ++ks) {
+    fa_r[ks] = dtc<N>(8 * it + r, 4 * ks + q);
+    fb_s[ks] = dtc<N>(8 * jt + r, 4 * ks + q);
+    fa_t[ks] = dtc<N>(4 * ks + q, 8 * it + r);
+    fb_t[ks] = dtc<N>(4 * ks + q, 8 * jt + r);
+  }
+
+  double acc_sq = 0.0;
+  for (int64_t m = 0; m < mine; ++m) {
+    const int64_t e = elem(m);
+    mbar_wait(ubar, (uint32_t)(m & 1));
+    const double *ust = ust0 + u_lead(e);
+    if (!u_bulk_ok(e)) {
+      for (int x = lt; x < NP; x += T) ust0[u_lead(e) + x] = u[e * NP + x];
+      named_bar_sync(1 + grp, T);
+    }
+    // ut for every k from the own columns (2N independent DFMA chains)
+    double t0[N], t1[N];
+    {
+      double uc0[N], uc1[N];
+#pragma unroll
+      for (int l = 0; l < N; ++l) {
+        uc0[l] = v0 ? ust[i0 + N * j + N2 * l] : 0.0;
+        uc1[l] = v1 ? ust[i0 + 1 + N * j + N2 * l] : 0.0;
+      }
+#pragma unroll
+      for (int k = 0; k < N; ++k) t0[k] = t1[k] = 0.0;
+#pragma unroll
+      for (int l = 0; l < N; ++l) {
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+          const double dk = c_dtc[N][k + N * l];
+          t0[k] = __fma_rn(dk, uc0[l], t0[k]);
+          t1[k] = __fma_rn(dk, uc1[l], t1[k]);
+        }
+      }
+    }
+
+    double wt0[N], wt1[N], p0[N], p1[N];
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      const int64_t s = m * N + k;
+      // ---- phase 1, slice k: ur^T / us^T from the staged u (row stride N)
+      double r0 = 0.0, r1 = 0.0, s0 = 0.0, s1 = 0.0;
+#pragma unroll
+      for (int ks = 0; ks < KT; ++ks) {
+        dmma(r0, r1, ust[(4 * ks + q) + N * (8 * jt + r) + N2 * k],
+             fa_r[ks]);
+        dmma(s0, s1, fb_s[ks],
+             ust[(8 * it + r) + N * (4 * ks + q) + N2 * k]);
+      }
+      if (k % KS == 0)
+        mbar_wait(&gbar[(s / KS) % SGS], (uint32_t)((s / KS / SGS) & 1));
+      const double *gs = slabs + (size_t)((s / KS) % SGS) * KS * C::SLAB +
+                         (size_t)(k % KS) * C::SLAB;
+      double *wr_k = wrr + (k & 1) * SL;
+      double *ws_k = wsr + (k & 1) * SL;
+      if (v0) {
+        const double2 *g2 =
+            reinterpret_cast<const double2 *>(gs + 6 * (i0 + N * j));
+        const double2 g01 = g2[0], g23 = g2[1], g45 = g2[2];
+        wr_k[i0 + P * j] = comb3<true>(g01.x, r0, g01.y, s0, g23.x, t0[k]);
+        ws_k[i0 + P * j] = comb3<true>(g01.y, r0, g23.y, s0, g45.x, t0[k]);
+        wt0[k] = comb3<true>(g23.x, r0, g45.x, s0, g45.y, t0[k]);
+      } else {
+        wt0[k] = 0.0;
+      }
+      if (v1) {
+        const double2 *g2 =
+            reinterpret_cast<const double2 *>(gs + 6 * (i0 + 1 + N * j));
+        const double2 g01 = g2[0], g23 = g2[1], g45 = g2[2];
+        wr_k[i0 + 1 + P * j] =
+            comb3<true>(g01.x, r1, g01.y, s1, g23.x, t1[k]);
+        ws_k[i0 + 1 + P * j] =
+            comb3<true>(g01.y, r1, g23.y, s1, g45.x, t1[k]);
+        wt1[k] = comb3<true>(g23.x, r1, g45.x, s1, g45.y, t1[k]);
+      } else {
+        wt1[k] = 0.0;
+      }
+      named_bar_sync(1 + grp, T);  // wr / ws of slice k complete
+      if (k % KS == KS - 1) {       // slab consumed: refill
+        const int64_t slab = s / KS;
+        if (lt == 0 && slab + SGS < nslabs) {
+          fence_proxy_async_smem();
+          issue_slab(slab + SGS);
+        }
+      }
+      if (k == N - 1 && lt == 0 && m + 1 < mine) {
+        fence_proxy_async_smem();
+        issue_u(m + 1);  // u consumed by every warp (barrier above)
+      }
+      // ---- phase 2 sums over wr / ws of slice k (tensor cores)
+      double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+      for (int ks = 0; ks < KT; ++ks) {
+        dmma(a0, a1, wr_k[(4 * ks + q) + P * (8 * jt + r)], fa_t[ks]);
+        dmma(a0, a1, fb_t[ks], ws_k[(8 * it + r) + P * (4 * ks + q)]);
+      }
+      p0[k] = a0;
+      p1[k] = a1;
+    }
+    // ---- the own-column sum over wt (needs every slice), then w
+    double *we = w + e * NP;
+#pragma unroll
+    for (int l = 0; l < N; ++l) {
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        const double dk = c_dtc[N][l + N * k];
+        p0[k] = __fma_rn(dk, wt0[l], p0[k]);
+        p1[k] = __fma_rn(dk, wt1[l], p1[k]);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      if (N % 2 == 0 && v1) {
+        *reinterpret_cast<double2 *>(we + i0 + N * j + N2 * k) =
+            make_double2(p0[k], p1[k]);
+      } else {
+        if (v0) we[i0 + N * j + N2 * k] = p0[k];
+        if (v1) we[i0 + 1 + N * j + N2 * k] = p1[k];
+      }
+      if constexpr (SUMSQ) {
+        if (v0) acc_sq = dadd(acc_sq, dmul(p0[k], p0[k]));
+        if (v1) acc_sq = dadd(acc_sq, dmul(p1[k], p1[k]));
+      }
+    }
+  }
+
+  if constexpr (SUMSQ) block_sumsq_partial(acc_sq, partials);
+}
+
+template <int N, int G, int SGS, int KS>
+static int launch_tc2(double *w, const double *u, const double *d,
+                      const double *g, int64_t nelt, const lfb_launch *geom,
+                      cudaStream_t s, int64_t *grid_out) {
+  using L = Tc2Smem<N, G, SGS, KS>;
+  static_assert(L::total <= 227 * 1024, "smem");
+  int sms = sm_count(geom);
+  if (sms <= 0) sms = 148;
+  const int per_sm = (geom && geom->ctas_per_sm > 0) ? geom->ctas_per_sm : 1;
+  int64_t grid64 = (int64_t)sms * per_sm;
+  if (grid64 * G > nelt) grid64 = (nelt + G - 1) / G;
+  const int grid = (int)(grid64 < 1 ? 1 : grid64);
+  if (grid_out) {
+    *grid_out = grid;
+    return LFB_OK;
+  }
+  const bool sumsq = geom && geom->sumsq;
+  if (sumsq && (!geom->workspace || geom->workspace_len < grid))
+    return fail(LFB_ERR_ARG, "semlap: sumsq workspace too small");
+  auto k = sumsq ? semlap_tc2_kernel<N, G, SGS, KS, true>
+                 : semlap_tc2_kernel<N, G, SGS, KS, false>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)L::total);
+  {
+    std::unique_lock<std::mutex> lk;
+    bool capturing = false;
+    int slot = N;
+    if (int rc = dconst_acquire(c_dtc, 256 * 8, 3, &slot, d, N, s, &lk,
+                                &capturing))
+      return rc;
+    k<<<grid, G * TcCfg<N>::T, L::total, s>>>(
+        w, u, g, nelt, sumsq ? geom->workspace : nullptr);
+    dconst_release(3, slot, s, capturing);
+  }
+  if (int rc = check_launch("lfb_semlap_f64(dmma2)")) return rc;
+  return sumsq ? sem_sumsq_finish(geom->workspace, grid, geom->sumsq, s)
+               : LFB_OK;
+}
+
+// }}}
+
 template <int N, int G, int SGS, int KS>
 static int launch_tc(double *w, const double *u, const double *d,
                      const double *g, int64_t nelt, const lfb_launch *geom,
@@ -383,6 +665,24 @@ static int launch_tc(double *w, const double *u, const double *d,
   X(15, 51, 1, 4, 1)    \
   X(16, 51, 1, 2, 2)
 
+// variant 52: the interleaved-phase kernel (groups, slab ring, slices/slab),
+// tuned per n on B200 (3 groups = 12 warps/SM beat 2 despite small spills
+// up to n = 15); 53: alternatives
+#define LFB_TC2_TABLE(X) \
+  X(9, 52, 3, 3, 1)      \
+  X(10, 52, 3, 2, 2)     \
+  X(11, 52, 3, 3, 1)     \
+  X(12, 52, 3, 2, 2)     \
+  X(13, 52, 3, 2, 1)     \
+  X(14, 52, 3, 2, 1)     \
+  X(15, 52, 3, 2, 1)     \
+  X(16, 52, 2, 4, 1)     \
+  X(12, 53, 2, 3, 2)     \
+  X(13, 53, 2, 3, 1)     \
+  X(14, 53, 2, 3, 1)     \
+  X(15, 53, 2, 3, 1)     \
+  X(16, 53, 2, 3, 1)
+
 int sem_tc_dispatch(int n, int variant, double *w, const double *u,
                     const double *d, const double *g, int64_t nelt,
                     const lfb_launch *geom, cudaStream_t s,
@@ -391,6 +691,11 @@ int sem_tc_dispatch(int n, int variant, double *w, const double *u,
   if (n == NN && variant == VV)                                             \
     return launch_tc<NN, GG, SS, KK>(w, u, d, g, nelt, geom, s, grid_out);
   LFB_TC_TABLE(X)
+#undef X
+#define X(NN, VV, GG, SS, KK)                                               \
+  if (n == NN && variant == VV)                                             \
+    return launch_tc2<NN, GG, SS, KK>(w, u, d, g, nelt, geom, s, grid_out);
+  LFB_TC2_TABLE(X)
 #undef X
   return -1;
 }

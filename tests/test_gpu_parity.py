@@ -172,7 +172,8 @@ def test_semlap_ragged_and_guarded(cuda, block, nelt):
 
 @pytest.mark.parametrize("n,variant", [(n, 50) for n in range(2, 17)]
                          + [(n, 51) for n in range(9, 17)]
-                         + [(n, 61) for n in (7, 9, 10, 11, 12)])
+                         + [(n, 61) for n in (7, 9, 10, 11, 12)]
+                         + [(n, 52) for n in range(9, 17)])
 def test_semlap_fma_mode(cuda, n, variant):
     """variant 50: the default kernel with every multiply-add fused (DFMA);
     variant 51: the FP64 tensor-core (DMMA) kernel for even n >= 10.
