@@ -633,15 +633,18 @@ def other_bench(args, local):
                   "parity": "bitwise" if args.variant in (1, 3) else
                   "tolerance (split-j, 1e-12 normwise)"})
         if args.variant == 0:
-            # the bitwise kernel is bound by each row's chain of n dependent
-            # DADDs (~17 cycles each on B200), not by HBM
+            # the bitwise kernel: each row is a chain of n dependent DADDs
+            # (8.1 cycles each, tools/micro/dadd_latency.cu) that overlaps
+            # the stream only partly
             r2 = run_rotating([lfb.Launcher(knl, e, variant=3).launch
                                for e in envs], 8 * n * n + 16 * n, 2 * n * n)
             r["bitwise"] = {"variant": 3, "value": r2["roofline"]["achieved"],
                             "ms_per_step": r2["ms_per_step"],
                             "frac": r2["roofline"]["frac"],
-                            "bound": "latency: 4096 dependent DADDs per row",
-                            "chain_us_at_17_cycles": n * 17 / 1.965e3}
+                            "bound": "latency: 4096 dependent DADDs per "
+                                     "row (8.1 cycles each) + the stream, "
+                                     "partly overlapped",
+                            "chain_us": n * 8.1 / 1.965e3}
         return r
     if wl == "sgemm":
         m = n = l = args.gemm_n

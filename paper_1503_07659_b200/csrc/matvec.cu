@@ -49,22 +49,35 @@ struct MvSmem {
   static constexpr size_t total = xs_off + MV_STAGES * x_bytes;
 };
 
+// The consumer is software pipelined: a dependent DADD costs 8.1 cycles on
+// B200 (tools/micro/dadd_latency.cu), so the row chain alone needs
+// n x 8.1 cycles; the products of tile q + 1 (LDS + DMUL, independent) are
+// interleaved with the 64 chained DADDs of tile q in program order, so the
+// warp's in-order issue never waits on anything but the chain itself.  A
+// stage is released as soon as its products are in registers.  Measured:
+// the consumer's loop alone runs at 8.07 cycles per column
+// (tools/micro/chain_probe.cu) and the stream alone at 6.1 TB/s (22 us at
+// n = 4096), but together 35 us: the in-order consumer waits for tile q + 1
+// before it can chain tile q, so memory latency and the chain only partly
+// overlap.  The split-j kernel below is the default.
+template <int ROWS>
 __global__ void __launch_bounds__(64, 1)
     matvec_tma_kernel(const __grid_constant__ CUtensorMap tmap_a,
                       double *__restrict__ y, const double *__restrict__ x,
                       int n) {
+  constexpr int JT = MV_JT, ST = MV_STAGES;
   extern __shared__ __align__(1024) unsigned char smem[];
   uint64_t *full = reinterpret_cast<uint64_t *>(smem);
-  uint64_t *empty = full + MV_STAGES;
+  uint64_t *empty = full + ST;
   double *tiles = reinterpret_cast<double *>(smem + MvSmem::tiles_off);
   double *xs = reinterpret_cast<double *>(smem + MvSmem::xs_off);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int i0 = blockIdx.x * MV_ROWS;
-  const int ntiles = (n + MV_JT - 1) / MV_JT;
+  const int i0 = blockIdx.x * ROWS;
+  const int ntiles = (n + JT - 1) / JT;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < MV_STAGES; ++s) {
+    for (int s = 0; s < ST; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
@@ -77,41 +90,27 @@ __global__ void __launch_bounds__(64, 1)
       asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap_a) : "memory");
       const uint64_t pol = policy_evict_first();
       for (int q = 0; q < ntiles; ++q) {
-        const int s = q % MV_STAGES;
-        mbar_wait(&empty[s], ((q / MV_STAGES) & 1) ^ 1);
-        const int j0 = q * MV_JT;
-        const int jn = min(MV_JT, n - j0);
+        const int s = q % ST;
+        mbar_wait(&empty[s], ((q / ST) & 1) ^ 1);
+        const int j0 = q * JT;
+        const int jn = min(JT, n - j0);
         const uint32_t xb = (uint32_t)jn * 8;  // n even => multiple of 16
-        mbar_arrive_expect_tx(&full[s], (uint32_t)MvSmem::tile_bytes + xb);
+        mbar_arrive_expect_tx(&full[s], (uint32_t)(ROWS * JT * 8) + xb);
         asm volatile(
             "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::"
             "complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(
-                smem_u32(tiles + (size_t)s * MV_ROWS * MV_JT)),
+                smem_u32(tiles + (size_t)s * MV_ROWS * JT)),
             "l"(&tmap_a), "r"(i0), "r"(j0), "r"(smem_u32(&full[s])),
             "l"(pol)
             : "memory");
-        bulk_g2s(xs + s * MV_JT, x + j0, xb, &full[s]);
+        bulk_g2s(xs + s * JT, x + j0, xb, &full[s]);
       }
     }
     return;
   }
 
-  // consumer warp: lane owns row i0 + lane
-  double acc = 0.0;  // "s = 0" (an i32 literal stored into the f64 scalar)
-  for (int q = 0; q < ntiles; ++q) {
-    const int s = q % MV_STAGES;
-    mbar_wait(&full[s], (q / MV_STAGES) & 1);
-    const double *tile = tiles + (size_t)s * MV_ROWS * MV_JT;
-    const double *xt = xs + s * MV_JT;
-    const int jn = min(MV_JT, n - q * MV_JT);
-    if (jn == MV_JT) {
-#pragma unroll 16
-      for (int jj = 0; jj < MV_JT; ++jj)
-        acc = dadd(acc, dmul(tile[jj * MV_ROWS + lane], xt[jj]));
-    } else {
-      for (int jj = 0; jj < jn; ++jj)
-        acc = dadd(acc, dmul(tile[jj * MV_ROWS + lane], xt[jj]));
-    }
+  // consumer warp: lane owns row i0 + lane (lanes >= ROWS idle)
+  auto release = [&](int s) {
     __syncwarp();
     if (lane == 0) {
       fence_proxy_async_smem();
@@ -119,8 +118,53 @@ __global__ void __launch_bounds__(64, 1)
                        smem_u32(&empty[s]))
                    : "memory");
     }
+  };
+  const int r = lane < ROWS ? lane : 0;
+  double acc = 0.0;  // "s = 0" (an i32 literal stored into the f64 scalar)
+  const int nfull = n / JT;
+  double p[JT];
+  if (nfull > 0) {
+    mbar_wait(&full[0], 0);
+    const double *t0 = tiles, *x0 = xs;
+#pragma unroll
+    for (int jj = 0; jj < JT; ++jj) p[jj] = dmul(t0[jj * ROWS + r], x0[jj]);
+    release(0);
   }
-  if (i0 + lane < n) y[i0 + lane] = acc;
+  constexpr int LD = 4;  // load distance: LDS latency / DADD latency
+  for (int q = 0; q < nfull; ++q) {
+    const bool nxt = q + 1 < nfull;
+    const int sn = (q + 1) % ST;
+    if (nxt) mbar_wait(&full[sn], ((q + 1) / ST) & 1);
+    const double *tn = tiles + (size_t)sn * MV_ROWS * JT;
+    const double *xn = xs + sn * JT;
+    double la[LD], lx[LD];
+#pragma unroll
+    for (int d = 0; d < LD; ++d) {
+      la[d] = nxt ? tn[d * ROWS + r] : 0.0;
+      lx[d] = nxt ? xn[d] : 0.0;
+    }
+#pragma unroll
+    for (int jj = 0; jj < JT; ++jj) {
+      acc = dadd(acc, p[jj]);  // the reference's chain, column order
+      const double a_ = la[jj % LD], x_ = lx[jj % LD];
+      if (nxt && jj + LD < JT) {  // the load LD columns ahead
+        la[jj % LD] = tn[(jj + LD) * ROWS + r];
+        lx[jj % LD] = xn[jj + LD];
+      }
+      p[jj] = dmul(a_, x_);       // product of tile q + 1 (unused if none)
+    }
+    if (nxt) release(sn);
+  }
+  if (nfull < ntiles) {  // ragged last tile: exactly jn more terms
+    const int q = nfull, s = q % ST;
+    mbar_wait(&full[s], (q / ST) & 1);
+    const double *t = tiles + (size_t)s * MV_ROWS * JT, *xt = xs + s * JT;
+    const int jn = n - q * JT;
+    for (int jj = 0; jj < jn; ++jj)
+      acc = dadd(acc, dmul(t[jj * ROWS + r], xt[jj]));
+    release(s);
+  }
+  if (lane < ROWS && i0 + lane < n) y[i0 + lane] = acc;
 }
 
 // {{{ split-j kernel (default; variant 2 forces it): tolerance parity, HBM
@@ -307,10 +351,29 @@ static int matvec_impl(double *y, const double *a, const double *x, int n,
           tm, y, x, n);
       return check_launch("lfb_matvec_f64");
     }
-    cudaFuncSetAttribute(matvec_tma_kernel,
+    // bitwise TMA kernel: 32-row panels; variant 4: 28-row panels (147
+    // CTAs at n = 4096 -- measured 3 % slower)
+    const bool r32 = !(geom && geom->variant == 4);
+    if (!r32) {
+      CUtensorMap tm28;
+      cuuint32_t box28[2] = {28, MV_JT};
+      if (encode(&tm28, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2,
+                 const_cast<double *>(a), dims, strides, box28, estr,
+                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return fail(LFB_ERR_LAUNCH, "matvec: tensor map encode failed");
+      cudaFuncSetAttribute(matvec_tma_kernel<28>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)MvSmem::total);
+      matvec_tma_kernel<28><<<(n + 27) / 28, 64, MvSmem::total, s>>>(
+          tm28, y, x, n);
+      return check_launch("lfb_matvec_f64");
+    }
+    cudaFuncSetAttribute(matvec_tma_kernel<32>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)MvSmem::total);
-    matvec_tma_kernel<<<grid, 64, MvSmem::total, s>>>(tm, y, x, n);
+    matvec_tma_kernel<32><<<grid, 64, MvSmem::total, s>>>(tm, y, x, n);
   } else {
     matvec_direct_kernel<<<(n + 127) / 128, 128, 0, s>>>(y, a, x, n);
   }

@@ -306,10 +306,12 @@ def test_fill_misaligned_pointer(cuda):
     assert h[0] == 0 and (h[1:] == 2.0).all()
 
 
-@pytest.mark.parametrize("n", [4096, 128, 256, 1024 + 128])
+@pytest.mark.parametrize("n", [4096, 128, 256, 1024 + 128, 1000, 4094])
 def test_matvec(cuda, n):
-    """BASELINE config 2 at n=4096: full bitwise comparison."""
-    _r, knl = fx.translate(fx.matvec_source("f64"))
+    """BASELINE config 2 at n=4096: full bitwise comparison (ragged n: the
+    untransformed kernel, same entry point)."""
+    raw, knl = fx.translate(fx.matvec_source("f64"))
+    knl = knl if n % 128 == 0 else raw
     gen = torch.Generator(device=cuda).manual_seed(n)
     a = torch.rand(n * n, dtype=torch.float64, device=cuda, generator=gen)
     x = torch.rand(n, dtype=torch.float64, device=cuda, generator=gen)
@@ -318,6 +320,9 @@ def test_matvec(cuda, n):
     lfb.interpret(knl, env, inplace=True, variant=3)  # bitwise TMA kernel
     ref = oracle.matvec(np.zeros(n), a.cpu().numpy(), x.cpu().numpy(), n,
                         threads=8)
+    assert y.cpu().numpy().tobytes() == ref.tobytes()
+    y.fill_(float("nan"))
+    lfb.interpret(knl, env, inplace=True, variant=4)  # 28-row panels
     assert y.cpu().numpy().tobytes() == ref.tobytes()
     y.fill_(float("nan"))
     lfb.interpret(knl, env, inplace=True, variant=1)  # bitwise direct loads
