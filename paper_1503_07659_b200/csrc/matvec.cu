@@ -59,7 +59,9 @@ struct MvSmem {
 // (tools/micro/chain_probe.cu) and the stream alone at 6.1 TB/s (22 us at
 // n = 4096), but together 35 us: the in-order consumer waits for tile q + 1
 // before it can chain tile q, so memory latency and the chain only partly
-// overlap.  The split-j kernel below is the default.
+// overlap (a variant that hands the products to a separate chain warp
+// through a shared-memory ring measured the same, 36 us).  The split-j
+// kernel below is the default.
 template <int ROWS>
 __global__ void __launch_bounds__(64, 1)
     matvec_tma_kernel(const __grid_constant__ CUtensorMap tmap_a,
@@ -351,8 +353,8 @@ static int matvec_impl(double *y, const double *a, const double *x, int n,
           tm, y, x, n);
       return check_launch("lfb_matvec_f64");
     }
-    // bitwise TMA kernel: 32-row panels; variant 4: 28-row panels (147
-    // CTAs at n = 4096 -- measured 3 % slower)
+    // bitwise TMA kernel: 32-row panels (variant 3 / default for n < 256);
+    // variant 4: 28-row panels (147 CTAs at n = 4096, measured 3 % slower)
     const bool r32 = !(geom && geom->variant == 4);
     if (!r32) {
       CUtensorMap tm28;

@@ -324,6 +324,7 @@ def test_matvec(cuda, n):
     y.fill_(float("nan"))
     lfb.interpret(knl, env, inplace=True, variant=4)  # 28-row panels
     assert y.cpu().numpy().tobytes() == ref.tobytes()
+
     y.fill_(float("nan"))
     lfb.interpret(knl, env, inplace=True, variant=1)  # bitwise direct loads
     assert y.cpu().numpy().tobytes() == ref.tobytes()
