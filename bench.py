@@ -323,9 +323,12 @@ def sem_bench(args, rank, world, local):
                                  / (1 << 21)),
                      "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": bytes_per_launch,
-                     "kernel": f"semlap_kc_kernel variant {sem_variant} "
-                               "(1 launch per step, after a 512 B d -> "
-                               "constant-bank copy)",
+                     "kernel": ("semlap_tc2_kernel (FP64 DMMA tensor "
+                                "cores + DFMA, interleaved phases)"
+                                if sem_variant == 50 and n == 8 else
+                                f"semlap variant {sem_variant}")
+                               + ": 1 launch per step, after a d -> "
+                               "constant-bank copy",
                      "stream_probe_gbs": probe_gbs,
                      "stream_probe_note": "same buffers, same bytes, no "
                                           "arithmetic (lfb_probe_stream)"},

@@ -271,14 +271,16 @@ static int launch_kc(double *w, const double *u, const double *d,
                : LFB_OK;
 }
 
-// (n, variant) -> (G, SG, fma).  -1: no constant-bank entry.  Variant 50 =
-// the default configuration in FMA mode (semlap_common.cuh).
+// (n, variant) -> (G, SG, fma).  -1: no constant-bank entry.  Variant 55 =
+// the default configuration in DFMA mode (semlap_common.cuh); the DFMA-mode
+// default at n = 8 (variant 50) is the DMMA kernel (semlap_tc.cu), which
+// draws less power in sustained runs.
 #define LFB_KC_TABLE(X) \
   X(8, 0, 4, 1, false)  \
   X(8, 40, 4, 1, false) \
   X(8, 41, 5, 1, false) \
   X(8, 42, 3, 2, false) \
-  X(8, 50, 4, 1, true)
+  X(8, 55, 4, 1, true)
 
 int sem_kc_dispatch(int n, int variant, double *w, const double *u,
                     const double *d, const double *g, int64_t nelt,

@@ -45,7 +45,7 @@ __constant__ double c_dtc[17][256];  // d(a,b) at [N][a + N b]
 
 template <int N>
 struct TcCfg {
-  static constexpr int NT = 2;               // 8-wide tiles per direction
+  static constexpr int NT = (N + 7) / 8;     // 8-wide tiles per direction
   static constexpr int W = NT * NT;          // warps per element
   static constexpr int T = 32 * W;
   static constexpr int KT = (N + 3) / 4;     // k-steps of 4
@@ -350,7 +350,7 @@ struct Tc2Smem {
   static constexpr size_t grp_doubles =
       (size_t)UST + (size_t)SGS * KS * C::SLAB + 4 * (size_t)C::SL;
   static constexpr size_t grp_bytes = (grp_doubles * 8 + 127) / 128 * 128;
-  static constexpr size_t bars = 256;
+  static constexpr size_t bars = 512;  // up to 64 mbarriers
   static constexpr size_t total = bars + G * grp_bytes;
 };
 
@@ -363,9 +363,9 @@ __global__ void __launch_bounds__(G *TcCfg<N>::T, 1)
   using L = Tc2Smem<N, G, SGS, KS>;
   constexpr int NP = C::NP, T = C::T, KT = C::KT, P = C::P, SL = C::SL;
   constexpr int N2 = N * N;
-  static_assert(N > 8 && N <= 16, "n = 9..16");
+  static_assert(N >= 8 && N <= 16, "n = 8..16");
   static_assert(N % KS == 0, "KS divides n");
-  static_assert(G * (1 + SGS) <= 32, "mbarriers");
+  static_assert(G * (1 + SGS) <= 64 && G <= 15, "mbarriers, barrier ids");
 
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t *bars = reinterpret_cast<uint64_t *>(smem);
@@ -669,6 +669,8 @@ static int launch_tc(double *w, const double *u, const double *d,
 // tuned per n on B200 (3 groups = 12 warps/SM beat 2 despite small spills
 // up to n = 15); 53: alternatives
 #define LFB_TC2_TABLE(X) \
+  X(8, 52, 6, 4, 2)      \
+  X(8, 53, 7, 4, 2)      \
   X(9, 52, 3, 3, 1)      \
   X(10, 52, 3, 2, 2)     \
   X(11, 52, 3, 3, 1)     \

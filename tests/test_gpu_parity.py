@@ -101,7 +101,7 @@ def test_semlap_o7_65536_elements(cuda):
                [(0, 1024), (30000, 31000), (nelt - 1024, nelt)])
 
 
-@pytest.mark.parametrize("variant", [1, 2, 3, 4, 5, 6, 7, 9, 10, 11, 12, 13, 14, 15, 16, 17, 18, 19, 39, 40, 41, 42])
+@pytest.mark.parametrize("variant", [1, 2, 3, 4, 5, 6, 7, 9, 10, 11, 12, 13, 14, 15, 16, 17, 18, 19, 39, 40, 41, 42])  # bitwise ones
 def test_semlap_o7_variants(cuda, variant):
     nelt = 4096
     _sem_check(8, nelt, fx.semlap_source(8), cuda, [(0, nelt)],
@@ -173,7 +173,8 @@ def test_semlap_ragged_and_guarded(cuda, block, nelt):
 @pytest.mark.parametrize("n,variant", [(n, 50) for n in range(2, 17)]
                          + [(n, 51) for n in range(9, 17)]
                          + [(n, 61) for n in (7, 9, 10, 11, 12)]
-                         + [(n, 52) for n in range(9, 17)])
+                         + [(n, 52) for n in range(8, 17)] + [(8, 53),
+                                                              (8, 55)])
 def test_semlap_fma_mode(cuda, n, variant):
     """variant 50: the default kernel with every multiply-add fused (DFMA);
     variant 51: the FP64 tensor-core (DMMA) kernel for even n >= 10.
