@@ -608,18 +608,19 @@ static int sem_dispatch(double *w, const double *u, const double *d,
     if (rc != -1) return rc;
   }
   if (var0 == 60 || var0 == 61 ||
-      (var0 == 50 && (n == 7 || n == 9 || n == 10))) {
+      (var0 == 50 && (n == 9 || n == 10))) {
     // two k-columns per thread (semlap_gen2.cu), n = 7, 9..12; the DFMA-mode
-    // default at n = 7, 9, 10 (+2..6 % over one column per thread)
+    // default at n = 9, 10 (+2..5 % over one column per thread)
     const int rc = sem_gen2_dispatch(n, var0 == 50 ? 61 : var0, w, u, d, g,
                                      nelt, geom, s, grid_out);
     if (rc != -1) return rc;
   }
-  if ((var0 >= 51 && var0 <= 53) || (var0 == 50 && (n == 8 || n >= 12))) {
+  if ((var0 >= 51 && var0 <= 53) ||
+      (var0 == 50 && (n == 7 || n == 8 || n >= 12))) {
     // FP64 tensor cores (semlap_tc.cu), n = 8..16; the interleaved-phase
     // kernel (52) is the DFMA-mode default for n >= 12, where it beats the
-    // column kernels by 12-28 %, and at n = 8, where it matches them in
-    // isolation and stays 8 % faster under the sustained power cap
+    // column kernels by 12-28 %, at n = 7 (+11 %), and at n = 8, where it
+    // matches them in isolation and stays 8 % faster under the power cap
     const int rc = sem_tc_dispatch(n, var0 == 50 ? 52 : var0, w, u, d, g,
                                    nelt, geom, s, grid_out);
     if (rc != -1) return rc;

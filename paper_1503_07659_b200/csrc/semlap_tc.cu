@@ -363,7 +363,7 @@ __global__ void __launch_bounds__(G *TcCfg<N>::T, 1)
   using L = Tc2Smem<N, G, SGS, KS>;
   constexpr int NP = C::NP, T = C::T, KT = C::KT, P = C::P, SL = C::SL;
   constexpr int N2 = N * N;
-  static_assert(N >= 8 && N <= 16, "n = 8..16");
+  static_assert(N >= 7 && N <= 16, "n = 7..16");
   static_assert(N % KS == 0, "KS divides n");
   static_assert(G * (1 + SGS) <= 64 && G <= 15, "mbarriers, barrier ids");
 
@@ -669,6 +669,7 @@ static int launch_tc(double *w, const double *u, const double *d,
 // tuned per n on B200 (3 groups = 12 warps/SM beat 2 despite small spills
 // up to n = 15); 53: alternatives
 #define LFB_TC2_TABLE(X) \
+  X(7, 52, 12, 4, 1)     \
   X(8, 52, 6, 4, 2)      \
   X(8, 53, 7, 4, 2)      \
   X(9, 52, 3, 3, 1)      \

@@ -173,7 +173,7 @@ def test_semlap_ragged_and_guarded(cuda, block, nelt):
 @pytest.mark.parametrize("n,variant", [(n, 50) for n in range(2, 17)]
                          + [(n, 51) for n in range(9, 17)]
                          + [(n, 61) for n in (7, 9, 10, 11, 12)]
-                         + [(n, 52) for n in range(8, 17)] + [(8, 53),
+                         + [(n, 52) for n in range(7, 17)] + [(8, 53),
                                                               (8, 55)])
 def test_semlap_fma_mode(cuda, n, variant):
     """variant 50: the default kernel with every multiply-add fused (DFMA);
