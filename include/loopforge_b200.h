@@ -165,6 +165,16 @@ int lfb_module_load(const void *cubin, int64_t len, const char *kernel_name,
 int lfb_module_launch(lfb_module m, const int64_t *grid, const int32_t *block,
                       int32_t smem, void **args, lfb_stream stream);
 int lfb_module_unload(lfb_module m);
+/* Tensor map (TMA descriptor, 128 bytes into *map) for a precompute
+ * footprint of a column-major argument array (transforms.py:669-674 gives the
+ * box): dtype 0 f64, 1 f32, 2 i32; dims[rank] extents (dim 0 contiguous),
+ * strides_bytes[rank-1] for dims 1.., box[rank], swizzle 0/32/64/128.
+ * LFB_ERR_UNSUPPORTED when the array violates the tensor-map rules (16-B
+ * aligned base and strides); the generated kernel then fetches
+ * cooperatively. */
+int lfb_tmap_encode(void *map, int dtype, int rank, const int64_t *dims,
+                    const int64_t *strides_bytes, const int32_t *box,
+                    int swizzle_bytes, const void *base);
 
 /* Microbenchmark used by bench.py to state the FP64 issue ceiling the SEM
  * kernel runs against: iters x 8 independent DMUL+DADD chains per thread. */

@@ -64,6 +64,8 @@ SIGNATURES = {
     "lfb_module_launch": [P, C.POINTER(C.c_int64), C.POINTER(C.c_int32),
                           C.c_int32, C.POINTER(P), P],
     "lfb_module_unload": [P],
+    "lfb_tmap_encode": [P, I32, I32, C.POINTER(C.c_int64),
+                        C.POINTER(C.c_int64), C.POINTER(C.c_int32), I32, P],
 }
 _RESTYPES = {"lfb_last_error": C.c_char_p, "lfb_semlap_workspace": C.c_int64,
              "lfb_sgemm_workspace": C.c_int64}

@@ -84,6 +84,12 @@ struct Driver {
                      unsigned, unsigned, unsigned, CUstream, void **,
                      void **) = nullptr;
   CUresult (*err_string)(CUresult, const char **) = nullptr;
+  CUresult (*encode_tiled)(CUtensorMap *, CUtensorMapDataType, cuuint32_t,
+                           void *, const cuuint64_t *, const cuuint64_t *,
+                           const cuuint32_t *, const cuuint32_t *,
+                           CUtensorMapInterleave, CUtensorMapSwizzle,
+                           CUtensorMapL2promotion,
+                           CUtensorMapFloatOOBfill) = nullptr;
   bool ok = false;
   std::string why;
 };
@@ -111,6 +117,7 @@ Driver &driver() {
     LFB_DRV(func_set_attr, cuFuncSetAttribute)
     LFB_DRV(launch, cuLaunchKernel)
     LFB_DRV(err_string, cuGetErrorString)
+    LFB_DRV(encode_tiled, cuTensorMapEncodeTiled)
 #undef LFB_DRV
     d.ok = true;
   });
@@ -225,6 +232,72 @@ int lfb_module_launch(lfb_module m, const int64_t *grid, const int32_t *block,
                         (unsigned)block[1], (unsigned)block[2],
                         (unsigned)smem, (CUstream)stream, args, nullptr);
   if (r != CUDA_SUCCESS) return drv_fail("cuLaunchKernel", r);
+  return LFB_OK;
+}
+
+int lfb_tmap_encode(void *map, int dtype, int rank, const int64_t *dims,
+                    const int64_t *strides_bytes, const int32_t *box,
+                    int swizzle_bytes, const void *base) {
+  using namespace lfb;
+  if (!map || !dims || !box || !base || (rank > 1 && !strides_bytes))
+    return fail(LFB_ERR_ARG, "lfb_tmap_encode: null argument");
+  if (rank < 1 || rank > 5)
+    return fail(LFB_ERR_UNSUPPORTED, "lfb_tmap_encode: rank %d", rank);
+  static const CUtensorMapDataType types[] = {
+      CU_TENSOR_MAP_DATA_TYPE_FLOAT64, CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+      CU_TENSOR_MAP_DATA_TYPE_INT32};
+  static const int esize[] = {8, 4, 4};
+  if (dtype < 0 || dtype > 2)
+    return fail(LFB_ERR_ARG, "lfb_tmap_encode: dtype %d", dtype);
+  // the tensor-map rules, checked here so an unsuitable footprint is an
+  // UNSUPPORTED status (the caller then runs the kernel's cooperative fetch)
+  if (reinterpret_cast<uintptr_t>(base) % 16)
+    return fail(LFB_ERR_UNSUPPORTED, "tensor map: base not 16-B aligned");
+  cuuint64_t gdim[5], gstride[4];
+  cuuint32_t bdim[5], estride[5];
+  for (int d = 0; d < rank; ++d) {
+    if (dims[d] < 1 || dims[d] >= (int64_t(1) << 31) || box[d] < 1 ||
+        box[d] > 256)
+      return fail(LFB_ERR_UNSUPPORTED, "tensor map: dim %d extent %lld box %d",
+                  d, (long long)dims[d], box[d]);
+    gdim[d] = (cuuint64_t)dims[d];
+    bdim[d] = (cuuint32_t)box[d];
+    estride[d] = 1;
+    if (d > 0) {
+      int64_t st = strides_bytes[d - 1];
+      if (st <= 0 || st % 16 || st >= (int64_t(1) << 40))
+        return fail(LFB_ERR_UNSUPPORTED,
+                    "tensor map: stride %lld B of dim %d not a positive "
+                    "multiple of 16", (long long)st, d);
+      gstride[d - 1] = (cuuint64_t)st;
+    }
+  }
+  if ((box[0] * esize[dtype]) % 16)
+    return fail(LFB_ERR_UNSUPPORTED, "tensor map: inner box %d B",
+                box[0] * esize[dtype]);
+  CUtensorMapSwizzle sw;
+  switch (swizzle_bytes) {
+    case 0: sw = CU_TENSOR_MAP_SWIZZLE_NONE; break;
+    case 32: sw = CU_TENSOR_MAP_SWIZZLE_32B; break;
+    case 64: sw = CU_TENSOR_MAP_SWIZZLE_64B; break;
+    case 128: sw = CU_TENSOR_MAP_SWIZZLE_128B; break;
+    default:
+      return fail(LFB_ERR_ARG, "lfb_tmap_encode: swizzle %d", swizzle_bytes);
+  }
+  Driver &d = driver();
+  if (!d.ok) return fail(LFB_ERR_LAUNCH, "%s", d.why.c_str());
+  alignas(64) CUtensorMap tm;
+  CUresult r = d.encode_tiled(&tm, types[dtype], (cuuint32_t)rank,
+                              const_cast<void *>(base), gdim, gstride, bdim,
+                              estride, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    const char *str = "unknown";
+    if (d.err_string) d.err_string(r, &str);
+    return fail(LFB_ERR_UNSUPPORTED, "cuTensorMapEncodeTiled: %s", str);
+  }
+  memcpy(map, &tm, sizeof(tm));
   return LFB_OK;
 }
 

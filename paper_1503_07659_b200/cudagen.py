@@ -49,11 +49,18 @@ CT = {I32: "int", F32: "float", F64: "double"}
 PRELUDE = r"""
 typedef long long i64;
 typedef unsigned int u32;
-static __device__ __forceinline__ i64 lfb_floordiv(i64 a, i64 b) {
+/* index arithmetic width: int when every array, parameter and work-group
+   count fits (the reference's emitted C uses int throughout), else 64-bit;
+   the launcher picks the build (generic.py) */
+#ifndef LFB_IX
+#define LFB_IX long long
+#endif
+typedef LFB_IX lfb_ix;
+static __device__ __forceinline__ lfb_ix lfb_floordiv(lfb_ix a, lfb_ix b) {
   return (a >= 0 ? a : a - b + 1) / b;  /* b > 0 */
 }
-static __device__ __forceinline__ i64 lfb_max(i64 a, i64 b) { return a > b ? a : b; }
-static __device__ __forceinline__ i64 lfb_min(i64 a, i64 b) { return a < b ? a : b; }
+static __device__ __forceinline__ lfb_ix lfb_max(lfb_ix a, lfb_ix b) { return a > b ? a : b; }
+static __device__ __forceinline__ lfb_ix lfb_min(lfb_ix a, lfb_ix b) { return a < b ? a : b; }
 static __device__ __forceinline__ int lfb_ipow(int b, int e) {
   int r = 1;
   for (; e > 0; --e) r = (int)((u32)r * (u32)b);
@@ -66,6 +73,47 @@ template <typename T> static __device__ __forceinline__ T lfb_npmax(T a, T b) {
   return (a != a) ? a : ((b != b) ? b : (b > a ? b : a));
 }
 """
+
+TMA_PRELUDE = r"""
+/* precompute footprints by TMA (SURVEY.md §8(f) row 3) */
+struct __align__(64) lfb_tmap { unsigned long long v[16]; };
+static __device__ __forceinline__ unsigned lfb_smem(const void *p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+static __device__ __forceinline__ void lfb_bar_init(unsigned long long *bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(lfb_smem(bar)));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+static __device__ __forceinline__ void lfb_expect_tx(unsigned long long *bar,
+                                                     unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+               :: "r"(lfb_smem(bar)), "r"(bytes) : "memory");
+}
+static __device__ __forceinline__ void lfb_bar_wait(unsigned long long *bar,
+                                                    unsigned ph) {
+  unsigned done = 0;
+  while (!done)
+    asm volatile("{\n .reg .pred p;\n"
+                 " mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+                 " selp.u32 %0, 1, 0, p;\n}"
+                 : "=r"(done) : "r"(lfb_smem(bar)), "r"(ph) : "memory");
+}
+"""
+
+
+def _tma_fn(rank):
+    cs = ", ".join(f"int c{i}" for i in range(rank))
+    regs = ", ".join(f"%{i + 2}" for i in range(rank))
+    ops = ", ".join(f'"r"(c{i})' for i in range(rank))
+    return (f"static __device__ __forceinline__ void lfb_tma{rank}(void *dst, "
+            f"const lfb_tmap *m, {cs}, unsigned long long *bar) {{\n"
+            f'  asm volatile("cp.async.bulk.tensor.{rank}d.shared::cluster.'
+            f"global.tile.mbarrier::complete_tx::bytes [%0], [%1, {{{regs}}}],"
+            f' [%{rank + 2}];"\n'
+            f'               :: "r"(lfb_smem(dst)), '
+            f'"l"((unsigned long long)m), {ops}, "r"(lfb_smem(bar)) '
+            f': "memory");\n}}\n')
+
 
 NVRTC_OPTIONS = ("--gpu-architecture=sm_100a", "--fmad=false",
                  "--std=c++17", "-default-device", "-lineinfo")
@@ -100,13 +148,14 @@ def _lit_float(v, t):
 
 
 def _aff(a):
-    """AffineExpr -> i64 C expression."""
+    """AffineExpr -> index-typed C expression."""
     parts = []
     for name in sorted(a.coeffs):
         c = a.coeffs[name]
-        parts.append(f"(i64)({name})" if c == 1 else f"{c}LL * (i64)({name})")
+        parts.append(f"(lfb_ix)({name})" if c == 1
+                     else f"{c} * (lfb_ix)({name})")
     if a.constant or not parts:
-        parts.append(f"({a.constant}LL)")
+        parts.append(f"({a.constant})")
     return "(" + " + ".join(parts) + ")"
 
 
@@ -114,10 +163,10 @@ def _bound(b):
     if b.divisor == 1:
         return _aff(b.numerator + b.offset)
     if b.exact:
-        core = f"({_aff(b.numerator)} / {b.divisor}LL)"
+        core = f"({_aff(b.numerator)} / {b.divisor})"
     else:
-        core = f"lfb_floordiv({_aff(b.numerator)}, {b.divisor}LL)"
-    return f"({core} + {b.offset}LL)" if b.offset else core
+        core = f"lfb_floordiv({_aff(b.numerator)}, {b.divisor})"
+    return f"({core} + {b.offset})" if b.offset else core
 
 
 def _combine(texts, fn):
@@ -136,6 +185,31 @@ def _temp_strides(shape):
 
 
 @dataclass
+class TmaMap:
+    """A precompute footprint fetched by TMA: the tensor map the launcher
+    encodes for argument *array* (lfb_tmap_encode)."""
+    array: str
+    dtype: str
+    box: tuple              # box extents per array dim (dim 0 contiguous)
+    swizzle: int            # 0 or 128 (bytes)
+
+
+@dataclass
+class _TmaPlan:
+    temp: str
+    array: str
+    esize: int
+    sdim: tuple             # temp dim -> array dim
+    fetch: tuple            # temp dim -> fetch iname
+    ext: tuple              # box extent per array dim
+    width: int              # inner-dim piece (elements)
+    pieces: int
+    rows: int               # product of the box extents of dims 1..
+    swizzle: int
+    coord: tuple            # array dim -> AffineExpr origin (fetch inames 0)
+
+
+@dataclass
 class Program:
     source: str
     entry: str
@@ -146,6 +220,7 @@ class Program:
     demoted: tuple          # workgroup temporaries demoted to per-thread
     cooperative: int        # fetch nests distributed over the CTA
     key: str                # content hash of the source
+    tma: tuple = ()         # tensor maps (TmaMap), kernel params after lfb_G*
 
 
 class _Emitter:
@@ -170,6 +245,14 @@ class _Emitter:
             else:
                 self.scalars.add(a.name)
         self.temp_shapes = {}
+        self.temp_alloc = {}
+        self.tma_plan = self._plan_tma(k)
+        self.tma_maps = []     # TmaMap per emitted footprint
+        self.tma_index = {}    # temp -> map index
+        self.pipes = 0         # double-buffered (prefetching) loops
+        self.pipe_runs = {}    # id(first fetch nest) -> (K, loop, plans)
+        self.pipe_buf = {}     # temp -> current-buffer variable
+        self.pipe_temps = set()
         for t in k.temporaries.values():
             self.dtypes[t.name] = t.dtype
             if t.shape:
@@ -181,9 +264,17 @@ class _Emitter:
                             "the CUDA emitter needs constant extents")
                     shape.append(s.constant)
                 self.temp_shapes[t.name] = tuple(shape)
+                alloc = list(shape)
+                if t.address_space == "workgroup" and len(shape) >= 2 \
+                        and shape[-1] % 2 == 0 and t.name not in self.tma_plan:
+                    # odd row pitch: work-items reading down a column of a
+                    # shared tile hit distinct banks (the layout of a
+                    # temporary is the executor's choice, interp.py:408-414)
+                    alloc[-1] += 1
+                self.temp_alloc[t.name] = alloc
                 self.arrays[t.name] = tuple(
                     polyset.AffineExpr.const(s)
-                    for s in _temp_strides(shape))
+                    for s in _temp_strides(alloc))
             else:
                 self.scalars.add(t.name)
         self.lines = []
@@ -191,6 +282,12 @@ class _Emitter:
         self.visible = list(self.parallel)
         self.tmp = 0
         self.cooperative = 0
+        self.promoted = {}    # array -> (subscript, register name)
+        self.n_promoted = 0
+        self.written = set()
+        for insn in k.instructions:
+            if isinstance(insn.lhs, ex.Subscript):
+                self.written.add(insn.lhs.array)
 
     # {{{ typed expressions (interp.py:140-256)
 
@@ -214,6 +311,9 @@ class _Emitter:
                 return n, self.dtypes[n]
             raise CodegenError(f"unbound name '{n}'")
         if isinstance(e, ex.Subscript):
+            hit = self.promoted.get(e.array)
+            if hit is not None and hit[0] == e:
+                return hit[1], self.dtypes[e.array]
             return f"{e.array}[{self.flat(e)}]", self.dtypes[e.array]
         if isinstance(e, ex.Compare):
             lt_, lt = self.rv(e.left)
@@ -322,7 +422,7 @@ class _Emitter:
             e.op, _lit_int(0, t))
         self.line(f"{ct} {acc} = {init};")
         self.line(f"int {first} = 1;")
-        self.line(f"for (i64 {e.iname} = {lo}; {e.iname} <= {up}; "
+        self.line(f"for (lfb_ix {e.iname} = {lo}; {e.iname} <= {up}; "
                   f"++{e.iname}) {{")
         self.ind += 1
         self.lines.extend(inner)
@@ -348,6 +448,8 @@ class _Emitter:
         return acc, t
 
     def flat(self, e):
+        if e.array in self.tma_plan:
+            return self._tma_flat(e)
         strides = self.arrays.get(e.array)
         if strides is None:
             raise CodegenError(f"no strides known for array '{e.array}'")
@@ -358,7 +460,7 @@ class _Emitter:
                 it = _aff(aff)
             else:
                 txt, _t = self.rv(idx)
-                it = f"((i64)({txt}))"
+                it = f"((lfb_ix)({txt}))"
             parts.append(it if stride == polyset.AffineExpr.const(1)
                          else f"{_aff(stride)} * {it}")
         return " + ".join(parts) if parts else "0"
@@ -485,10 +587,10 @@ class _Emitter:
         if self.k.iname_tags.get(node.iname) == "unroll":
             self.line("#pragma unroll")
         if strided:
-            self.line(f"for (i64 {node.iname} = {lo} + lfb_tid; "
+            self.line(f"for (lfb_ix {node.iname} = {lo} + lfb_tid; "
                       f"{node.iname} <= {up}; {node.iname} += lfb_nthreads) {{")
         else:
-            self.line(f"for (i64 {node.iname} = {lo}; {node.iname} <= {up}; "
+            self.line(f"for (lfb_ix {node.iname} = {lo}; {node.iname} <= {up}; "
                       f"++{node.iname}) {{")
         self.ind += 1
         self.visible.append(node.iname)
@@ -504,8 +606,11 @@ class _Emitter:
         tgt = insn.lhs.name if isinstance(insn.lhs, ex.VarRef) \
             else insn.lhs.array
         rhs, rt = self.rv(insn.rhs)
+        hit = self.promoted.get(tgt)
         if isinstance(insn.lhs, ex.VarRef):
             lhs = insn.lhs.name
+        elif hit is not None and hit[0] == insn.lhs:
+            lhs = hit[1]
         else:
             lhs = f"{insn.lhs.array}[{self.flat(insn.lhs)}]"
         self.line(f"{lhs} = {_cast(rhs, rt, self.dtypes[tgt])};  "
@@ -519,8 +624,26 @@ class _Emitter:
         if isinstance(node, codegen.Block):
             self.walk_children(node.children, ctx)
         elif isinstance(node, codegen.Loop):
-            self.emit_loop(node, lambda: self.walk_children(node.children,
-                                                            ctx))
+            if ctx["guard"] == "stmt" and not (
+                    ctx["wg"] and self._touches(node, ctx["wg"])[0]):
+                # no shared writes inside, so no barriers: the residual
+                # guard can enclose the whole nest instead of every statement
+                self.line("if (lfb_in) {")
+                self.ind += 1
+                self.walk(node, dict(ctx, guard=None))
+                self.ind -= 1
+                self.line("}")
+                return
+            pipe = self._pipeline(node, ctx)
+            if pipe is not None:
+                self._emit_pipelined(node, ctx, *pipe)
+                return
+            promo = self._promotions(node)
+            if promo:
+                self._emit_promoted(node, ctx, promo)
+            else:
+                self.emit_loop(node, lambda: self.walk_children(
+                    node.children, ctx))
         elif isinstance(node, codegen.Conditional):
             cond = " && ".join(f"!{f}" if neg else f"({f} != 0)"
                                for f, neg in sorted(node.predicates))
@@ -531,6 +654,425 @@ class _Emitter:
             self.line("}")
         else:
             self.emit_stmt(self.imap[node.insn_id], ctx["guard"] == "stmt")
+
+    # {{{ precompute footprints by TMA
+
+    def _plan_tma(self, k):
+        """Workgroup temporaries whose one fetch instruction is a plain copy
+        of a rectangular box of a column-major argument -- what ``precompute``
+        builds (transforms.py:541-684: temporary extents = footprint box,
+        fetch ``T[f0, f1, ..] = A[base + f..]``).  Such a tile can be loaded
+        by one thread with the Tensor Memory Accelerator instead of by every
+        work-item; the temporary is then laid out the way TMA writes it (the
+        array's contiguous dimension innermost, 128-B rows swizzled so
+        column reads stay conflict-free)."""
+        plan = {}
+        args = {a.name: a for a in k.args}
+        writers = {}
+        for insn in k.instructions:
+            if isinstance(insn.lhs, ex.Subscript):
+                writers.setdefault(insn.lhs.array, []).append(insn)
+        written = set(writers)
+        for t in k.temporaries.values():
+            if t.address_space != "workgroup" or not t.shape or \
+                    len(writers.get(t.name, ())) != 1:
+                continue
+            if not all(s.is_constant() for s in t.shape):
+                continue
+            shape = [s.constant for s in t.shape]
+            insn = writers[t.name][0]
+            lhs, rhs = insn.lhs, insn.rhs
+            if not all(isinstance(i, ex.VarRef) for i in lhs.index):
+                continue
+            fetch = tuple(i.name for i in lhs.index)
+            if len(set(fetch)) != len(fetch) or \
+                    not isinstance(rhs, ex.Subscript):
+                continue
+            a = args.get(rhs.array)
+            if a is None or a.kind != "global-array" or a.name in written \
+                    or a.dtype != t.dtype or not 1 <= len(a.shape) <= 5:
+                continue
+            if a.strides[0] != polyset.AffineExpr.const(1):
+                continue
+            esize = 8 if t.dtype == F64 else 4
+            sdim = [None] * len(fetch)
+            ext = [1] * len(a.shape)
+            coord = []
+            ok = len(rhs.index) == len(a.shape)
+            for d, idx in enumerate(rhs.index if ok else ()):
+                aff = ex.expression_to_affine(idx)
+                if aff is None:
+                    ok = False
+                    break
+                here = [f for f in fetch if aff.coeff(f) != 0]
+                if len(here) > 1 or any(aff.coeff(f) != 1 for f in here):
+                    ok = False
+                    break
+                if here:
+                    tdim = fetch.index(here[0])
+                    sdim[tdim] = d
+                    ext[d] = shape[tdim]
+                coord.append(aff.substitute({f: polyset.AffineExpr.const(0)
+                                             for f in here}))
+            if not ok or None in sdim or ext[0] * esize % 16 or \
+                    any(e > 256 for e in ext[1:]):
+                continue
+            rows = 1
+            for e in ext[1:]:
+                rows *= e
+            # swizzle only if some consumer's work-items differ along a
+            # non-contiguous dim (a column read down 128-B rows: bank
+            # conflicts); reads whose work-items vary only along the
+            # contiguous dim are conflict-free in the dense layout
+            local = {i for i, tg in k.iname_tags.items()
+                     if (tg or "").startswith("l.")}
+            strided = False
+            for other in k.instructions:
+                if other is insn:
+                    continue
+                for e in other.read_expressions():
+                    for sub in self._subscripts(e):
+                        if sub.array != t.name:
+                            continue
+                        for tdim, idx in enumerate(sub.index):
+                            if sdim[tdim] != 0 and \
+                                    ex.free_variables(idx) & local:
+                                strided = True
+            width, swz = ext[0], 0
+            if strided and ext[0] * esize % 128 == 0 and rows % 8 == 0:
+                width, swz = 128 // esize, 128     # 128-B rows, swizzled
+            elif ext[0] > 256:
+                continue
+            plan[t.name] = _TmaPlan(t.name, a.name, esize, tuple(sdim), fetch,
+                                    tuple(ext), width, ext[0] // width, rows,
+                                    swz, tuple(coord))
+        return plan
+
+    def _tma_flat(self, e):
+        """Element offset of a TMA-laid-out temporary: pieces of *width*
+        along the array's contiguous dim, each a dense [rows][width] block,
+        128-B swizzle on top."""
+        p = self.tma_plan[e.array]
+        v = ["0"] * len(p.ext)
+        for tdim, idx in enumerate(e.index):
+            aff = ex.expression_to_affine(idx)
+            if aff is not None:
+                txt = _aff(aff)
+            else:
+                txt, _t = self.rv(idx)
+            v[p.sdim[tdim]] = f"(int)({txt})"
+        row = v[-1] if len(v) > 1 else "0"
+        for d in range(len(v) - 2, 0, -1):
+            row = f"({v[d]} + {p.ext[d]} * {row})"
+        if p.pieces > 1:
+            sh = p.width.bit_length() - 1
+            inner = f"(int)((unsigned)({v[0]}) & {p.width - 1}u)"
+            piece = (f" + {p.width * p.rows} * "
+                     f"(int)((unsigned)({v[0]}) >> {sh})")
+        else:
+            inner, piece = f"({v[0]})", ""
+        if p.swizzle:
+            # 128-B swizzle (16-B chunk ^= row mod 8) written on the
+            # (inner, row) split, so the row term hoists out of loops over
+            # the contiguous index: (inner ^ ((row & 7) << s)) + width*row
+            s_ = 1 if p.esize == 8 else 2
+            inner = f"(({inner}) ^ ((({row}) & 7) << {s_}))"
+        buf = self.pipe_buf.get(e.array)
+        if buf is not None:
+            piece += f" + {p.ext[0] * p.rows} * {buf}"
+        return f"({inner} + {p.width} * {row}{piece})"
+
+    def _tma_nest(self, node):
+        """The plan of a cooperative fetch nest TMA can replace: a perfect
+        nest over exactly the plan's fetch inames, each from 0 with a
+        constant upper candidate equal to the temporary's extent (the
+        footprint box; a tighter domain clip only shortens what the
+        reference fetches -- the consumers never read past it)."""
+        if not isinstance(node, codegen.Loop):
+            return None
+        loops, cur = [], node
+        while isinstance(cur, codegen.Loop):
+            loops.append(cur)
+            if len(cur.children) != 1:
+                break
+            cur = cur.children[0]
+        last = loops[-1]
+        if len(last.children) != 1 or \
+                not isinstance(last.children[0], codegen.Statement):
+            return None
+        insn = self.imap[last.children[0].insn_id]
+        if not isinstance(insn.lhs, ex.Subscript):
+            return None
+        p = self.tma_plan.get(insn.lhs.array)
+        if p is None or sorted(l.iname for l in loops) != sorted(p.fetch):
+            return None
+        shape = self.temp_shapes[p.temp]
+        vis = len(self.visible)
+        try:
+            for lp in loops:
+                lo, up = codegen.loop_bounds(self.k, lp.iname, self.visible)
+                if not lo or not all(b.is_plain_affine() and
+                                     b.as_affine().is_constant() and
+                                     b.as_affine().constant == 0 for b in lo):
+                    return None
+                ext = shape[p.fetch.index(lp.iname)]
+                if not any(b.is_plain_affine() and b.as_affine().is_constant()
+                           and b.as_affine().constant == ext - 1 for b in up):
+                    return None
+                self.visible.append(lp.iname)
+        finally:
+            del self.visible[vis:]
+        return p
+
+    def _emit_tma_issue(self, plans, cond="lfb_tid == 0", bar="0", buf=None,
+                        subst=None):
+        """One elected work-item arms barrier *bar* with the byte count and
+        issues one TMA per 128-B piece of every footprint (into buffer
+        *buf* of a double-buffered tile; *subst* shifts the loop iname for
+        a prefetch)."""
+        total = sum(p.esize * p.ext[0] * p.rows for p in plans)
+        self.line(f"if ({cond}) {{")
+        self.ind += 1
+        self.line(f"lfb_expect_tx(&lfb_bars[{bar}], {total}u);")
+        for p in plans:
+            if p.temp not in self.tma_index:
+                self.tma_index[p.temp] = len(self.tma_maps)
+                box = (p.width,) + p.ext[1:]
+                self.tma_maps.append(TmaMap(p.array, self.dtypes[p.array],
+                                            box, p.swizzle))
+            m = self.tma_index[p.temp]
+            rank = len(p.ext)
+            self.tma_ranks.add(rank)
+            coord = [c.substitute(subst) if subst else c for c in p.coord]
+            for piece in range(p.pieces):
+                cs = [f"(int)({_aff(c)})" for c in coord]
+                if piece:
+                    cs[0] = f"(int)({_aff(coord[0])} + {piece * p.width})"
+                off = str(piece * p.width * p.rows)
+                if buf is not None:
+                    off = f"{off} + {p.ext[0] * p.rows} * ({buf})"
+                self.line(f"lfb_tma{rank}(&{p.temp}[{off}], &lfb_tm{m}, "
+                          f"{', '.join(cs)}, &lfb_bars[{bar}]);")
+        self.ind -= 1
+        self.line("}")
+
+    def _pipeline(self, node, ctx):
+        """Double-buffer the TMA tiles of a sequential loop whose body
+        starts a writer run of TMA-fetchable footprints that move with the
+        loop's iname (the paper's k_outer): the next iteration's tiles are
+        prefetched into the other buffer while this one is consumed.  Legal
+        because the fetched arrays are never written by the kernel."""
+        wg = ctx["wg"]
+        if not wg or not self.tma_plan:
+            return None
+        kids = node.children
+        i = 0
+        while i < len(kids):
+            w, r = self._touches(kids[i], wg)
+            if w and not r:
+                break
+            i += 1
+        if i == len(kids):
+            return None
+        j = i
+        while j < len(kids):
+            w, r = self._touches(kids[j], wg)
+            if not w or r:
+                break
+            j += 1
+        self.visible.append(node.iname)
+        try:
+            plans = []
+            for c in kids[i:j]:
+                if not self._cooperative(c, wg):
+                    return None
+                p = self._tma_nest(c)
+                if p is None:
+                    return None
+                plans.append(p)
+        finally:
+            self.visible.pop()
+        if not any(node.iname in c.variables for p in plans
+                   for c in p.coord):
+            return None
+        temps = {p.temp for p in plans}
+        inside = {self.imap[st.insn_id].id for st in self._walk_stmts(node)}
+        for insn in self.k.instructions:
+            if insn.id not in inside and (
+                    (self._reads(insn) | self._writes(insn)) & temps):
+                return None
+        for t in temps:
+            if t in self.pipe_temps:
+                return None
+        return kids[i], plans
+
+    def _walk_stmts(self, node):
+        if isinstance(node, codegen.Statement):
+            yield node
+        else:
+            for c in node.children:
+                yield from self._walk_stmts(c)
+
+    def _emit_pipelined(self, node, ctx, first, plans):
+        k = self.pipes
+        self.pipes += 1
+        lowers, uppers = codegen.loop_bounds(self.k, node.iname, self.visible)
+        lo = _combine([_bound(b) for b in lowers], "lfb_max")
+        up = _combine([_bound(b) for b in uppers], "lfb_min")
+        temps = {p.temp for p in plans}
+        self.pipe_temps |= temps
+        self.line("{")
+        self.ind += 1
+        self.line(f"const lfb_ix lfb_plo{k} = {lo}, lfb_pup{k} = {up};")
+        self.barrier()
+        self._emit_tma_issue(
+            plans, cond=f"lfb_tma && lfb_tid == 0 && lfb_plo{k} <= lfb_pup{k}",
+            bar="0", buf="0",
+            subst={node.iname: polyset.AffineExpr.var(f"lfb_plo{k}")})
+        self.line(f"for (lfb_ix {node.iname} = lfb_plo{k}; {node.iname} <= "
+                  f"lfb_pup{k}; ++{node.iname}) {{")
+        self.ind += 1
+        self.line(f"const int lfb_pb{k} = (int)(({node.iname} - lfb_plo{k}) "
+                  "& 1);")
+        self.visible.append(node.iname)
+        for t in temps:
+            self.pipe_buf[t] = f"lfb_pb{k}"
+        self.pipe_runs[id(first)] = (k, node, plans)
+        self.walk_children(node.children, ctx)
+        del self.pipe_runs[id(first)]
+        for t in temps:
+            del self.pipe_buf[t]
+        self.visible.pop()
+        self.ind -= 1
+        self.line("}")
+        self.ind -= 1
+        self.line("}")
+
+    # }}}
+
+    def _promotions(self, node):
+        """Global array elements a sequential loop updates in place --
+        ``c[i,j] = c[i,j] + ...`` with the subscript invariant in the loop
+        -- kept in a register across the loop (scalar replacement): one load
+        before, one store after, the same operations in the same order in
+        between, so results stay bitwise.  Only statements that are direct,
+        unconditional children of the loop qualify (then the element is
+        touched on every trip, so hoisting the load adds no access the
+        reference would not make), and every access to the array inside the
+        loop must use that one subscript (arguments never alias: each is its
+        own buffer)."""
+        direct = [self.imap[c.insn_id] for c in node.children
+                  if isinstance(c, codegen.Statement)]
+        cands = {}
+        for insn in direct:
+            lhs = insn.lhs
+            if isinstance(lhs, ex.Subscript) and lhs.array not in \
+                    self.temp_shapes and lhs.array not in self.promoted:
+                cands.setdefault(lhs.array, lhs)
+        if not cands:
+            return []
+        outer = set(self.visible) | self.params
+        out = []
+        for name, sub in cands.items():
+            fv = set()
+            for idx in sub.index:
+                fv |= ex.free_variables(idx)
+            if not fv <= outer or node.iname in fv:
+                continue
+            ok = True
+            for insn in self._stmts(node):
+                subs = [x for e in [insn.lhs] + insn.read_expressions()
+                        for x in self._subscripts(e) if x.array == name]
+                if not subs:
+                    continue
+                if insn not in direct or any(x != sub for x in subs):
+                    ok = False
+                    break
+            if ok:
+                out.append((name, sub))
+        return out
+
+    def _emit_promoted(self, node, ctx, promo):
+        lowers, uppers = codegen.loop_bounds(self.k, node.iname, self.visible)
+        lo = _combine([_bound(b) for b in lowers], "lfb_max")
+        up = _combine([_bound(b) for b in uppers], "lfb_min")
+        n = self.n_promoted
+        self.n_promoted += 1
+        self.line("{")
+        self.ind += 1
+        self.line(f"const lfb_ix lfb_lo{n} = {lo}, lfb_up{n} = {up};")
+        cond = f"lfb_lo{n} <= lfb_up{n}"
+        if ctx["guard"] == "stmt":
+            cond += " && lfb_in"
+        self.line(f"const bool lfb_run{n} = {cond};")
+        regs = []
+        for k, (name, sub) in enumerate(promo):
+            reg = f"lfb_r{n}_{k}"
+            self.line(f"{CT[self.dtypes[name]]} {reg};")
+            self.line(f"if (lfb_run{n}) {reg} = {name}[{self.flat(sub)}];")
+            regs.append((name, sub, reg))
+        for name, sub, reg in regs:
+            self.promoted[name] = (sub, reg)
+        full = self._full_trip(lowers, uppers, node, ctx)
+        if full is not None:
+            # interior work-groups run the footprint's full, constant trip:
+            # a fully unrolled copy (constant tile offsets fold into the
+            # addressing); edge groups take the general loop
+            self.line(f"if (lfb_lo{n} == {full[0]} && lfb_up{n} == "
+                      f"{full[1]}) {{")
+            self.ind += 1
+            self.line("#pragma unroll")
+            self.line(f"for (lfb_ix {node.iname} = {full[0]}; {node.iname} "
+                      f"<= {full[1]}; ++{node.iname}) {{")
+            self.ind += 1
+            self.visible.append(node.iname)
+            self.walk_children(node.children, ctx)
+            self.visible.pop()
+            self.ind -= 1
+            self.line("}")
+            self.ind -= 1
+            self.line("} else {")
+            self.ind += 1
+        if self.k.iname_tags.get(node.iname) == "unroll":
+            self.line("#pragma unroll")
+        self.line(f"for (lfb_ix {node.iname} = lfb_lo{n}; {node.iname} <= "
+                  f"lfb_up{n}; ++{node.iname}) {{")
+        self.ind += 1
+        self.visible.append(node.iname)
+        self.walk_children(node.children, ctx)
+        self.visible.pop()
+        self.ind -= 1
+        self.line("}")
+        if full is not None:
+            self.ind -= 1
+            self.line("}")
+        for name, sub, reg in regs:
+            del self.promoted[name]
+            self.line(f"if (lfb_run{n}) {name}[{self.flat(sub)}] = {reg};")
+        self.ind -= 1
+        self.line("}")
+
+    def _full_trip(self, lowers, uppers, node, ctx):
+        """(lo, hi) when the loop has constant lower bounds and a constant
+        upper candidate with a short trip (<= 64), a body of at most a few
+        statements and no shared-tile writes (so no barriers to duplicate);
+        None otherwise."""
+        def const(b):
+            return b.is_plain_affine() and b.as_affine().is_constant()
+        if not lowers or not all(const(b) for b in lowers):
+            return None
+        ups = [b.as_affine().constant for b in uppers if const(b)]
+        if not ups or len(ups) == len(uppers):
+            return None            # nothing to specialise, or no constant
+        lo = max(b.as_affine().constant for b in lowers)
+        hi = min(ups)
+        if not 1 <= hi - lo + 1 <= 64:
+            return None
+        if ctx["wg"] and self._touches(node, ctx["wg"])[0]:
+            return None
+        if sum(1 for _ in self._stmts(node)) > 4:
+            return None
+        return lo, hi
 
     def _touches(self, node, wg):
         w = r = False
@@ -558,12 +1100,50 @@ class _Emitter:
                         break
                     j += 1
                 self.barrier()
+                tma = []
                 for c2 in children[i:j]:
                     if self._cooperative(c2, wg):
                         self.cooperative += 1
+                        p = self._tma_nest(c2)
+                        if p is not None:
+                            tma.append((c2, p))
+                            continue
                         self._emit_strided(c2, ctx)
                     else:
                         self.walk(c2, ctx)
+                pipe = self.pipe_runs.get(id(children[i]))
+                if tma and pipe is not None:
+                    # double-buffered: prefetch the next iteration's tiles
+                    # into the other buffer, then wait for this one's
+                    k, loop, plans = pipe
+                    nxt = polyset.AffineExpr.var(loop.iname) + 1
+                    self.line("if (lfb_tma) {")
+                    self.ind += 1
+                    self._emit_tma_issue(
+                        plans, cond=f"lfb_tid == 0 && {loop.iname} + 1 <= "
+                                    f"lfb_pup{k}",
+                        bar=f"lfb_pb{k} ^ 1", buf=f"lfb_pb{k} ^ 1",
+                        subst={loop.iname: nxt})
+                    self.line(f"lfb_bar_wait(&lfb_bars[lfb_pb{k}], "
+                              f"(lfb_tph >> lfb_pb{k}) & 1u);")
+                    self.line(f"lfb_tph ^= 1u << lfb_pb{k};")
+                    self.ind -= 1
+                elif tma:
+                    # TMA when the launcher could encode every tensor map,
+                    # else the same tiles fetched cooperatively
+                    self.line("if (lfb_tma) {")
+                    self.ind += 1
+                    self._emit_tma_issue([p for _c, p in tma])
+                    self.line("lfb_bar_wait(&lfb_bars[0], lfb_tph & 1u);")
+                    self.line("lfb_tph ^= 1u;")
+                    self.ind -= 1
+                if tma:
+                    self.line("} else {")
+                    self.ind += 1
+                    for c2, _p in tma:
+                        self._emit_strided(c2, ctx)
+                    self.ind -= 1
+                    self.line("}")
                 self.barrier()
                 i = j
                 continue
@@ -606,6 +1186,32 @@ class _Emitter:
                             return outer.iname
         return inner.iname
 
+    def _const_box(self, outer, inner, b1, b2, fast):
+        """((lo, extent) slow, (lo, extent) fast) when both fetch inames have
+        constant lower bounds and a constant upper candidate (the footprint
+        box precompute sized the temporary with, transforms.py:669-674);
+        None otherwise."""
+        def const(bounds):
+            if not all(b.is_plain_affine() and b.as_affine().is_constant()
+                       for b in bounds):
+                return None
+            return [b.as_affine().constant for b in bounds]
+        res = {}
+        for node, (lo, up) in ((outer, b1), (inner, b2)):
+            los = const(lo)
+            ups = [b.as_affine().constant for b in up
+                   if b.is_plain_affine() and b.as_affine().is_constant()]
+            if not los or not ups:
+                return None
+            l0, u0 = max(los), min(ups)
+            if u0 < l0 or (u0 - l0 + 1) > 4096:
+                return None
+            res[node.iname] = (l0, u0 - l0 + 1)
+        slow = outer.iname if fast == inner.iname else inner.iname
+        if res[slow][1] * res[fast][1] > (1 << 20):
+            return None
+        return res[slow], res[fast]
+
     def _subscripts(self, e):
         if isinstance(e, ex.Subscript):
             yield e
@@ -623,16 +1229,42 @@ class _Emitter:
         fast = self._fast_iname(outer, inner)
         order = rng if fast == inner.iname else rng[::-1]
         (sn, slo, sup), (fn_, flo, fup) = order
+        box = self._const_box(outer, inner, b1, b2, fast)
         self.line("{")
         self.ind += 1
-        self.line(f"const i64 lfb_s{n} = {slo}, lfb_f{n} = {flo};")
-        self.line(f"const i64 lfb_ns{n} = lfb_max({sup} - lfb_s{n} + 1, 0LL);")
-        self.line(f"const i64 lfb_nf{n} = lfb_max({fup} - lfb_f{n} + 1, 0LL);")
-        self.line(f"for (i64 lfb_q{n} = lfb_tid; lfb_q{n} < lfb_ns{n} * "
+        if box is not None:
+            # constant footprint box (the temporary's extents): the flat
+            # index splits with constant divisors, the domain clip is a test
+            (ls, es), (lf, ef) = box
+            self.line(f"const lfb_ix lfb_us{n} = {sup}, lfb_uf{n} = {fup};")
+            # the CTA size is static (l.N extents): a fixed trip count the
+            # compiler unrolls, so every work-item's loads issue together
+            self.line("#pragma unroll")
+            self.line(f"for (int lfb_q{n} = (int)lfb_tid; lfb_q{n} < "
+                      f"{es * ef}; lfb_q{n} += {self.nthreads}) {{")
+            self.ind += 1
+            self.line(f"const lfb_ix {sn} = {ls} + lfb_q{n} / {ef};")
+            self.line(f"const lfb_ix {fn_} = {lf} + lfb_q{n} % {ef};")
+            self.line(f"if ({sn} <= lfb_us{n} && {fn_} <= lfb_uf{n}) {{")
+            self.ind += 1
+            self.visible += [outer.iname, inner.iname]
+            self.walk_children(inner.children, ctx)
+            del self.visible[-2:]
+            self.ind -= 1
+            self.line("}")
+            self.ind -= 1
+            self.line("}")
+            self.ind -= 1
+            self.line("}")
+            return
+        self.line(f"const lfb_ix lfb_s{n} = {slo}, lfb_f{n} = {flo};")
+        self.line(f"const lfb_ix lfb_ns{n} = lfb_max({sup} - lfb_s{n} + 1, 0);")
+        self.line(f"const lfb_ix lfb_nf{n} = lfb_max({fup} - lfb_f{n} + 1, 0);")
+        self.line(f"for (lfb_ix lfb_q{n} = lfb_tid; lfb_q{n} < lfb_ns{n} * "
                   f"lfb_nf{n}; lfb_q{n} += lfb_nthreads) {{")
         self.ind += 1
-        self.line(f"const i64 {sn} = lfb_s{n} + lfb_q{n} / lfb_nf{n};")
-        self.line(f"const i64 {fn_} = lfb_f{n} + lfb_q{n} % lfb_nf{n};")
+        self.line(f"const lfb_ix {sn} = lfb_s{n} + lfb_q{n} / lfb_nf{n};")
+        self.line(f"const lfb_ix {fn_} = lfb_f{n} + lfb_q{n} % lfb_nf{n};")
         self.visible += [outer.iname, inner.iname]
         self.walk_children(inner.children, ctx)
         del self.visible[-2:]
@@ -658,19 +1290,6 @@ class _Emitter:
             f"({_aff(c.expr)} {'==' if c.kind == 'eq' else '>='} 0)"
             for c in guards)
 
-        decl = []
-        for name in sorted(k.temporaries):
-            t = k.temporaries[name]
-            ct = CT[t.dtype]
-            if not t.shape:
-                decl.append(f"{ct} {name} = 0;")
-            else:
-                size = 1
-                for s in self.temp_shapes[name]:
-                    size *= s
-                q = "__shared__ " if name in shared else ""
-                decl.append(f"{q}{ct} {name}[{size}];")
-
         pro = []
         gnames = {}   # g axis -> iname
         block = [1, 1, 1]
@@ -680,7 +1299,7 @@ class _Emitter:
             if kind == "g":
                 gnames[int(axis)] = iname
                 continue
-            pro.append(f"const i64 {iname} = (i64)threadIdx.{comp};")
+            pro.append(f"const lfb_ix {iname} = (lfb_ix)threadIdx.{comp};")
             if kind == "l":
                 _lo, ups = codegen.loop_bounds(k, iname, [])
                 if not all(b.is_plain_affine() and b.as_affine().is_constant()
@@ -689,25 +1308,32 @@ class _Emitter:
                         f"l.{axis} iname '{iname}' needs a constant extent")
                 block[int(axis)] = min(b.as_affine().constant
                                        for b in ups) + 1
-        pro.append("const i64 lfb_tid = (i64)threadIdx.x + (i64)blockDim.x * "
-                   "((i64)threadIdx.y + (i64)blockDim.y * (i64)threadIdx.z);")
-        pro.append("const i64 lfb_nthreads = (i64)blockDim.x * blockDim.y * "
-                   "blockDim.z;")
+        pro.append("const lfb_ix lfb_tid = (lfb_ix)(threadIdx.x + blockDim.x * "
+                   "(threadIdx.y + blockDim.y * threadIdx.z));")
+        pro.append("const lfb_ix lfb_nthreads = (lfb_ix)(blockDim.x * blockDim.y * "
+                   "blockDim.z);")
+
+        self.nthreads = block[0] * block[1] * block[2]
 
         # work-groups in a grid-stride loop over a capped 1-D grid: the
         # logical g.0 x g.1 x g.2 space (extents lfb_G0..2) is walked by
         # persistent CTAs, so tiny work-groups do not leave the GPU
         # CTA-launch bound; barriers stay uniform (every thread of a CTA
         # walks the same groups), shared tiles get a barrier between groups
+        if not shared:
+            self.tma_plan = {}
+        self.tma_ranks = set()
         self.lines = []
         self.ind = 1
-        self.line("const i64 lfb_ng = lfb_G0 * lfb_G1 * lfb_G2;")
-        self.line("for (i64 lfb_g = (i64)blockIdx.x; lfb_g < lfb_ng; "
-                  "lfb_g += (i64)gridDim.x) {")
+        self.line("const lfb_ix lfb_ng = (lfb_ix)(lfb_G0 * lfb_G1 * lfb_G2);")
+        self.line("const lfb_ix lfb_g0 = (lfb_ix)lfb_G0, lfb_g1 = (lfb_ix)lfb_G1, "
+                  "lfb_g2 = (lfb_ix)lfb_G2;")
+        self.line("for (lfb_ix lfb_g = (lfb_ix)blockIdx.x; lfb_g < lfb_ng; "
+                  "lfb_g += (lfb_ix)gridDim.x) {")
         self.ind += 1
         for axis, iname in sorted(gnames.items()):
-            div = " * ".join(f"lfb_G{a}" for a in range(axis)) or "1"
-            self.line(f"const i64 {iname} = (lfb_g / ({div})) % lfb_G{axis};")
+            div = " * ".join(f"lfb_g{a}" for a in range(axis)) or "1"
+            self.line(f"const lfb_ix {iname} = (lfb_g / ({div})) % lfb_g{axis};")
         for name in sorted(k.temporaries):
             t = k.temporaries[name]
             if not t.shape:
@@ -729,6 +1355,23 @@ class _Emitter:
         self.line("}")
         body = self.lines
 
+        decl = []
+        for name in sorted(k.temporaries):
+            t = k.temporaries[name]
+            ct = CT[t.dtype]
+            if not t.shape:
+                decl.append(f"{ct} {name} = 0;")
+            else:
+                size = 1
+                for s in self.temp_alloc[name]:
+                    size *= s
+                if name in self.pipe_temps:
+                    size *= 2                  # double-buffered tile
+                q = "__shared__ " if name in shared else ""
+                if name in shared and name in self.tma_plan:
+                    q += "__align__(1024) "   # swizzle atoms, TMA dst
+                decl.append(f"{q}{ct} {name}[{size}];")
+
         params = tuple(sorted(k.param_names))
         sig, order = [], []
         for a in k.args:
@@ -747,6 +1390,26 @@ class _Emitter:
         for a in range(3):  # logical work-group extents (launch geometry)
             sig.append(f"i64 lfb_G{a}")
             order.append(f"lfb_G{a}")
+        prelude = PRELUDE
+        if self.tma_maps:
+            sig.append("int lfb_tma")
+            order.append("lfb_tma")
+            for m in range(len(self.tma_maps)):
+                sig.append(f"const __grid_constant__ lfb_tmap lfb_tm{m}")
+                order.append(f"lfb_tm{m}")
+            prelude += TMA_PRELUDE + "".join(
+                _tma_fn(r) for r in sorted(self.tma_ranks))
+            decl.append("__shared__ __align__(8) unsigned long long "
+                        "lfb_bars[2];")
+            decl.append("unsigned lfb_tph = 0;  /* phase bit per barrier */")
+            chk = " || ".join(f"(lfb_smem({t}) & 1023u)"
+                              for t in sorted(self.tma_index))
+            pro.append("if (lfb_tma && lfb_tid == 0) {")
+            pro.append(f"  if ({chk}) __trap();  /* TMA tiles misaligned */")
+            pro.append("  lfb_bar_init(&lfb_bars[0]);")
+            pro.append("  lfb_bar_init(&lfb_bars[1]);")
+            pro.append("}")
+            pro.append("__syncthreads();")
         nthreads = block[0] * block[1] * block[2]
         if nthreads > 1024:
             raise CodegenError(
@@ -754,7 +1417,7 @@ class _Emitter:
                 "1024 threads per CTA")
         entry = f"lfb_gen_{k.name}"
         src = "\n".join(
-            [PRELUDE,
+            [prelude,
              f'extern "C" __global__ void __launch_bounds__({nthreads})',
              f"{entry}({', '.join(sig)})", "{"]
             + ["  " + d for d in decl] + ["  " + p for p in pro]
@@ -762,7 +1425,7 @@ class _Emitter:
         key = hashlib.sha256(src.encode()).hexdigest()[:16]
         return Program(src, entry, tuple(order), params, tuple(block),
                        tuple(sorted(shared)), tuple(sorted(demoted)),
-                       self.cooperative, key)
+                       self.cooperative, key, tuple(self.tma_maps))
 
 
 def emit_cuda(kernel):
@@ -771,4 +1434,4 @@ def emit_cuda(kernel):
     return _Emitter(kernel).emit()
 
 
-__all__ = ["Program", "emit_cuda", "NVRTC_OPTIONS", "promote"]
+__all__ = ["Program", "TmaMap", "emit_cuda", "NVRTC_OPTIONS", "promote"]

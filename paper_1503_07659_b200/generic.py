@@ -33,34 +33,35 @@ def program_for(kernel):
     return prog
 
 
-def compile_program(prog):
-    """NVRTC -> sm_100a cubin (no device needed)."""
-    cub = _CUBINS.get(prog.key)
+def compile_program(prog, narrow=False):
+    """NVRTC -> sm_100a cubin (no device needed).  *narrow*: 32-bit index
+    arithmetic (``LFB_IX=int``), valid when every index fits (launcher)."""
+    cub = _CUBINS.get((prog.key, narrow))
     if cub is not None:
         return cub
     lib = abi.load()
-    opts = (C.c_char_p * len(NVRTC_OPTIONS))(
-        *[o.encode() for o in NVRTC_OPTIONS])
+    names = NVRTC_OPTIONS + (("-DLFB_IX=int",) if narrow else ())
+    opts = (C.c_char_p * len(names))(*[o.encode() for o in names])
     n = C.c_int64(0)
     abi.check(lib.lfb_rtc_compile(prog.source.encode(),
                                   f"{prog.entry}.cu".encode(), opts,
-                                  len(NVRTC_OPTIONS), None, C.byref(n)),
+                                  len(names), None, C.byref(n)),
               f"NVRTC {prog.entry}")
     buf = C.create_string_buffer(n.value)
     abi.check(lib.lfb_rtc_compile(prog.source.encode(),
                                   f"{prog.entry}.cu".encode(), opts,
-                                  len(NVRTC_OPTIONS), buf, C.byref(n)),
+                                  len(names), buf, C.byref(n)),
               f"NVRTC {prog.entry}")
     cub = buf.raw[:n.value]
-    _CUBINS[prog.key] = cub
+    _CUBINS[(prog.key, narrow)] = cub
     return cub
 
 
-def _module(prog, device_index):
-    key = (prog.key, device_index)
+def _module(prog, device_index, narrow):
+    key = (prog.key, device_index, narrow)
     mod = _MODULES.get(key)
     if mod is None:
-        cub = compile_program(prog)
+        cub = compile_program(prog, narrow)
         h = C.c_void_p()
         abi.check(abi.load().lfb_module_load(cub, len(cub),
                                              prog.entry.encode(),
@@ -93,24 +94,81 @@ class GenericLauncher:
         self.env = env
         self.program = program_for(kernel)
         self.geometry = launch_geometry(kernel, env.params)
+        self._narrow = {}
+
+    def narrow(self, env):
+        """32-bit index arithmetic when every flat array size, parameter
+        value and the work-group count stay below 2^31 (2^30 for the
+        parameters, which bound expressions combine)."""
+        key = (tuple(sorted(env.params.items())),
+               tuple(sorted((n, a.data.numel())
+                            for n, a in env.arrays.items())))
+        hit = self._narrow.get(key)
+        if hit is None:
+            lim = 1 << 31
+            g = self.geometry
+            ng = 1
+            for x in g.group_extent:
+                ng *= max(1, int(x))
+            hit = (all(abs(int(v)) < (1 << 30) for v in env.params.values())
+                   and all(a.data.numel() < lim for a in env.arrays.values())
+                   and ng < lim)
+            self._narrow[key] = hit
+        return hit
+
+    def tensor_maps(self, env):
+        """TMA descriptors of the program's precompute footprints
+        (cudagen._plan_tma) for *env*'s buffers.  All-or-nothing: when one
+        array breaks the tensor-map rules (odd leading dimension, unaligned
+        base) the kernel runs its cooperative fetch for every tile."""
+        lib = abi.load()
+        args = {a.name: a for a in self.kernel.args}
+        maps, ok = [], True
+        for m in self.program.tma:
+            a = args[m.array]
+            buf = (C.c_uint64 * 16)()
+            maps.append(buf)
+            if not ok:
+                continue
+            t = env.arrays[m.array].data
+            esize = t.element_size()
+            dims = [int(x.eval(env.params)) for x in a.shape]
+            strides = [int(x.eval(env.params)) * esize for x in a.strides[1:]]
+            rank = len(dims)
+            rc = lib.lfb_tmap_encode(
+                buf, {"f64": 0, "f32": 1, "i32": 2}[m.dtype], rank,
+                (C.c_int64 * rank)(*dims), (C.c_int64 * max(1, rank - 1))(
+                    *(strides or [0])), (C.c_int32 * rank)(*m.box),
+                m.swizzle, C.c_void_p(t.data_ptr()))
+            if rc == abi.LFB_ERR_UNSUPPORTED:
+                ok = False
+            else:
+                abi.check(rc, f"tensor map for '{m.array}'")
+        return maps, ok
 
     def launch(self, env=None, stream=None):
         env = env or self.env
         prog = self.program
         dev = env.device if env.device is not None else torch.device(
             "cuda", torch.cuda.current_device())
+        narrow = self.narrow(env)
         with torch.cuda.device(dev):
-            mod = _module(prog, dev.index)
+            mod = _module(prog, dev.index, narrow)
             if stream is None:
                 stream = torch.cuda.current_stream(dev).cuda_stream
         vals = []
         args = {a.name: a for a in self.kernel.args}
         geo = self.geometry
         gext = [max(1, int(x)) for x in geo.group_extent]
+        maps, tma_ok = self.tensor_maps(env) if prog.tma else ((), False)
         for name in prog.arg_order:
             a = args.get(name)
             if name.startswith("lfb_G"):       # logical work-group extents
                 vals.append(C.c_int64(gext[int(name[5:])]))
+            elif name == "lfb_tma":
+                vals.append(C.c_int32(1 if tma_ok else 0))
+            elif name.startswith("lfb_tm"):
+                vals.append(maps[int(name[6:])])
             elif a is None:                    # a parameter (int64)
                 vals.append(C.c_int64(int(env.params[name])))
             elif a.kind == "global-array":

@@ -44,8 +44,9 @@ FIXTURES = _fixture_kernels()
 @pytest.mark.parametrize("name,knl", FIXTURES, ids=[n for n, _ in FIXTURES])
 def test_emits_and_compiles_for_sm100a(name, knl):
     prog = emit_cuda(knl)
-    cubin = compile_program(prog)
-    assert cubin[:4] == b"\x7fELF"
+    for narrow in (False, True):    # 64-bit and 32-bit index builds
+        cubin = compile_program(prog, narrow)
+        assert cubin[:4] == b"\x7fELF"
     assert prog.entry in prog.source
 
 
@@ -55,7 +56,12 @@ def test_paper_dgemm_uses_shared_tiles_and_barriers():
     assert prog.shared == ("a_acc_0", "b_acc_0") and not prog.demoted
     assert prog.cooperative == 2          # both tile fetches spread over CTA
     assert prog.block == (8, 16, 1)       # l.0 = j_inner, l.1 = i_inner
-    assert "__shared__ double a_acc_0[512];" in prog.source
+    # 16 x 32 tile laid out as TMA writes it, two buffers
+    assert "__shared__ __align__(1024) double a_acc_0[1024];" in prog.source
+    # c[i,j] accumulated in a register across k_inner (scalar replacement)
+    assert "lfb_r0_0 = (lfb_r0_0 + " in prog.source
+    # constant footprint box: no 64-bit division in the fetch
+    assert "lfb_q0 < 512" in prog.source
     assert prog.source.count("__syncthreads();") >= 2
     # the guard became a per-statement predicate so barriers stay uniform
     assert "const bool lfb_in =" in prog.source
@@ -130,6 +136,24 @@ def test_generic_engine_matches_reference(name, which, cuda):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("name", ["gen_dgemm_m20_n12_l40", "gen_mvacc_n64",
+                                  "gen_transpose_n37_m21", "gen_cond_n300"])
+def test_generic_wide_index_build(name, cuda, monkeypatch):
+    """The 64-bit index build (chosen when an array or parameter passes
+    2^31) gives the same bits as the 32-bit one the small goldens use."""
+    from paper_1503_07659_b200 import generic
+    monkeypatch.setattr(generic.GenericLauncher, "narrow",
+                        lambda self, env: False)
+    g = Golden(name)
+    _raw, knl = g.kernels()
+    out = lfb.interpret(knl, _env(g, knl, cuda), engine="generic")
+    torch.cuda.synchronize()
+    for o in g.outputs():
+        assert out.arrays[o].data.cpu().numpy().tobytes() == \
+            g.out(o).tobytes(), f"{name}:{o}"
+
+
+@pytest.mark.gpu
 def test_auto_engine_routes_unrecognised_kernels(cuda):
     g = Golden("gen_mvacc_n64")
     _raw, knl = g.kernels()
@@ -141,17 +165,43 @@ def test_auto_engine_routes_unrecognised_kernels(cuda):
         g.out("y").tobytes()
 
 
+def test_precompute_footprints_become_tma_loads():
+    """the paper's DGEMM tiles (a_acc_0 16x32,
+    b_acc_0 32x8 from precompute) are fetched by TMA, one elected thread
+    per tile, 128-B swizzled rows (b split into two 128-B pieces)."""
+    _raw, knl = fx.translate(fx.gemm_source("f64"), "dgemm.f")
+    prog = emit_cuda(knl)
+    # a is read along its contiguous dim (dense rows), b down its columns
+    # (128-B swizzle, split into two 128-B pieces)
+    assert [(m.array, m.box, m.swizzle) for m in prog.tma] == \
+        [("a", (16, 32), 0), ("b", (16, 8), 128)]
+    # double-buffered over k_outer: prologue + prefetch, 3 TMAs each
+    assert prog.source.count("lfb_tma2(") == 3 + 3 + 1
+    assert "lfb_expect_tx(&lfb_bars[0], 6144u);" in prog.source
+    assert "__shared__ __align__(1024) double a_acc_0[1024];" in prog.source
+    assert prog.arg_order[-3:] == ("lfb_tma", "lfb_tm0", "lfb_tm1")
+    # sgemm: 16 floats = 64-B rows for a (no swizzle), 128-B rows for b
+    _raw, ks = fx.translate(fx.gemm_source("f32"), "sgemm.f")
+    assert [(m.array, m.box, m.swizzle) for m in emit_cuda(ks).tma] == \
+        [("a", (16, 32), 0), ("b", (32, 8), 128)]
+
+
 @pytest.mark.gpu
-def test_generic_dgemm_larger(cuda):
-    """The paper's DGEMM script at 256^3 with ragged tiles against a
-    sequential-k numpy restatement (c + (alpha*b)*a per k, f64)."""
-    m, n, l = 250, 120, 200
+@pytest.mark.parametrize("m,n,l,tma", [(250, 120, 200, True),
+                                       (251, 120, 200, False),
+                                       (64, 40, 96, True)])
+def test_generic_dgemm_larger(m, n, l, tma, cuda):
+    """The paper's DGEMM script with ragged tiles against a sequential-k
+    numpy restatement (c + (alpha*b)*a per k, f64).  Odd m breaks the
+    tensor-map stride rule: the same kernel then fetches cooperatively."""
+    from paper_1503_07659_b200.generic import GenericLauncher
     _raw, knl = fx.translate(fx.gemm_source("f64"), "dgemm.f")
     rng = np.random.default_rng(3)
     a, b, c = rng.random((m, l)), rng.random((l, n)), rng.random((m, n))
     env = lfb.make_device_env(knl, {"m": m, "n": n, "l": l},
                               {"a": a, "b": b, "c": c, "alpha": 1.5},
                               device=cuda)
+    assert GenericLauncher(knl, env).tensor_maps(env)[1] is tma
     got = lfb.get_output(lfb.interpret(knl, env, engine="generic"), "c")
     want = c.copy()
     for k in range(l):
