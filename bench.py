@@ -347,7 +347,8 @@ def sem_e2e(knl, n, nelt, dev, steps, chunk=1 << 17, variant=0):
     interpret() and reads the result w back.  ``all_inputs_per_step`` also
     re-uploads g and d every step (PCIe-bound).  The elements are processed
     in chunks (each chunk is an SEM problem on a slice; elements are
-    independent) on two streams so PCIe copies overlap the kernel."""
+    independent); copies in, the kernel and copies out run on three streams
+    so both PCIe directions and the kernel overlap."""
     import torch
 
     import paper_1503_07659_b200 as lfb
@@ -363,9 +364,14 @@ def sem_e2e(knl, n, nelt, dev, steps, chunk=1 << 17, variant=0):
             v.copy_(torch.empty(v.numel(), dtype=torch.float64, device=dev)
                     .uniform_(lo, 1.0, generator=gen))
     hd = (torch.rand(n * n, dtype=torch.float64) * 2 - 1).pin_memory()
-    streams = [torch.cuda.Stream(dev) for _ in range(2)]
+    # three engines kept busy at once: host->device copies, the kernel,
+    # device->host copies, each on its own stream, over a ring of R buffer
+    # slots (events order slot reuse), so the PCIe directions overlap each
+    # other as well as the kernel
+    R = 3
+    h2d, comp, d2h = (torch.cuda.Stream(dev) for _ in range(3))
     bufs = []
-    for _ in streams:
+    for _ in range(R):
         bufs.append({"u": torch.empty(chunk * np3, dtype=torch.float64,
                                       device=dev),
                      "g": torch.empty(6 * chunk * np3, dtype=torch.float64,
@@ -374,34 +380,48 @@ def sem_e2e(knl, n, nelt, dev, steps, chunk=1 << 17, variant=0):
                                       device=dev),
                      "d": torch.empty(n * n, dtype=torch.float64,
                                       device=dev)})
+    ev_in = [torch.cuda.Event() for _ in range(R)]
+    ev_k = [torch.cuda.Event() for _ in range(R)]
+    ev_out = [torch.cuda.Event() for _ in range(R)]
     chunks = [(s, min(nelt, s + chunk)) for s in range(0, nelt, chunk)]
     launches = [0]
     resident = {}  # mode "resident": g and d uploaded once, kept on device
 
     def step():
         for c, (e0, e1) in enumerate(chunks):
-            st, b = streams[c % 2], bufs[c % 2]
+            sl, b = c % R, bufs[c % R]
             m = e1 - e0
-            with torch.cuda.stream(st):
+            with torch.cuda.stream(h2d):
+                h2d.wait_event(ev_k[sl])          # slot's inputs consumed
                 b["u"][:m * np3].copy_(hu[e0 * np3:e1 * np3],
                                        non_blocking=True)
-                if resident:
-                    gd = resident["g"][6 * e0 * np3:6 * e1 * np3]
-                    dd = resident["d"]
-                else:
+                if not resident:
                     b["g"][:6 * m * np3].copy_(hg[6 * e0 * np3:6 * e1 * np3],
                                                non_blocking=True)
                     b["d"].copy_(hd, non_blocking=True)
-                    gd, dd = b["g"], b["d"]
+                ev_in[sl].record(h2d)
+            if resident:
+                gd = resident["g"][6 * e0 * np3:6 * e1 * np3]
+                dd = resident["d"]
+            else:
+                gd, dd = b["g"], b["d"]
+            with torch.cuda.stream(comp):
+                comp.wait_event(ev_in[sl])
+                comp.wait_event(ev_out[sl])       # slot's result copied out
                 env = lfb.env_from_buffers(
                     knl, {"nelt": m}, {"u": b["u"], "g": gd,
                                        "w": b["w"], "d": dd})
                 lfb.interpret(knl, env, inplace=True, variant=variant)
                 launches[0] += 1
+                ev_k[sl].record(comp)
+            with torch.cuda.stream(d2h):
+                d2h.wait_event(ev_k[sl])
                 hw[e0 * np3:e1 * np3].copy_(b["w"][:m * np3],
                                             non_blocking=True)
+                ev_out[sl].record(d2h)
 
     cur = torch.cuda.current_stream(dev)
+    streams = (h2d, comp, d2h)
 
     def run(k):
         for s in streams:
@@ -451,7 +471,8 @@ def sem_e2e(knl, n, nelt, dev, steps, chunk=1 << 17, variant=0):
             "steps": steps, "gpu_launches": launches[0],
             "api": "paper_1503_07659_b200.interpret -> lfb_semlap_f64 "
                    f"(ctypes C-ABI), {len(chunks)} chunks of {chunk} "
-                   "elements on 2 streams",
+                   "elements; H2D, kernel and D2H on three streams over "
+                   f"{R} buffer slots",
             "inputs": "the operator's parameters g (geometric factors) and d "
                       "stay device-resident like a model's weights "
                       "(uploaded once, before the timed region); every step "
@@ -802,6 +823,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-nelt", type=int, default=0)
+    ap.add_argument("--e2e-chunk", type=int, default=1 << 17,
+                    help="elements per host<->device chunk in the e2e run")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.variant is None and args.workload not in ("sem2m", "sem65k"):
@@ -862,6 +885,7 @@ def main():
         except Exception:
             pass
         e2e = sem_e2e(knl, args.npts, nelt_e2e, dev, steps=3,
+                      chunk=args.e2e_chunk,
                       variant=res["config"]["variant"])
         ms = max_over_ranks(e2e["ms_per_step"], world)
         e2e["value"] = nelt_e2e * world * args.npts ** 3 / (ms * 1e-3) / 1e9
