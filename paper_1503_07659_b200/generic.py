@@ -156,9 +156,14 @@ class GenericLauncher:
             mod = _module(prog, dev.index, narrow)
             if stream is None:
                 stream = torch.cuda.current_stream(dev).cuda_stream
+        geo = self.geometry
+        if any(int(x) <= 0 for x in geo.group_extent):
+            # an empty g.N range: the reference's loop over it runs no
+            # iterations (the residual guard omits what launch sizing
+            # guarantees, so launching one group anyway would be wrong)
+            return
         vals = []
         args = {a.name: a for a in self.kernel.args}
-        geo = self.geometry
         gext = [max(1, int(x)) for x in geo.group_extent]
         maps, tma_ok = self.tensor_maps(env) if prog.tma else ((), False)
         for name in prog.arg_order:
