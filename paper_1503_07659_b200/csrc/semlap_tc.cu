@@ -35,6 +35,10 @@
 // stride P = 20 doubles: the fragment loads of a half warp hit 16 distinct
 // 8-byte bank slots), and wr / ws for the whole element in the same padded
 // layout.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <string.h>
+
 #include "dconst.cuh"
 #include "lfb_common.cuh"
 #include "semlap_common.cuh"
@@ -343,31 +347,53 @@ __global__ void __launch_bounds__(G *TcCfg<N>::T, 1)
 // staged u (zeroed smem makes every padded read finite), and 2-3 groups
 // (8-12 warps) fit per SM.  Arithmetic as variant 51 (DFMA mode, within
 // 1e-12; the phase-2 sums are added in a different order).
-template <int N, int G, int SGS, int KS>
+template <int N, int G, int SGS, int KS, bool SWZ = false>
 struct Tc2Smem {
   using C = TcCfg<N>;
-  static constexpr int UST = (C::NP + 2 + 1) / 2 * 2;  // + 8-byte lead
+  // SWZ (n = 16): u staged by a 2-D TMA with the 128-B swizzle, no lead
+  static constexpr int UST = SWZ ? C::NP : (C::NP + 2 + 1) / 2 * 2;
   static constexpr size_t grp_doubles =
       (size_t)UST + (size_t)SGS * KS * C::SLAB + 4 * (size_t)C::SL;
-  static constexpr size_t grp_bytes = (grp_doubles * 8 + 127) / 128 * 128;
-  static constexpr size_t bars = 512;  // up to 64 mbarriers
-  static constexpr size_t total = bars + G * grp_bytes;
+  static constexpr size_t galign = SWZ ? 1024 : 128;  // swizzle atoms
+  static constexpr size_t grp_bytes =
+      (grp_doubles * 8 + galign - 1) / galign * galign;
+  static constexpr size_t bars = SWZ ? 1024 : 512;  // up to 64 mbarriers
+  static constexpr size_t total = bars + G * grp_bytes + (SWZ ? 1024 : 0);
 };
 
-template <int N, int G, int SGS, int KS, bool SUMSQ>
+// index of u(c, R) in the staged element, R = j + N k the row: plain, or
+// (n = 16) the TMA 128-B swizzle -- 16-byte chunk c/2 of row R XOR R mod 8 --
+// which spreads the ur^T fragment (8 rows x 4 columns) over all banks
+// instead of 4 (the row stride of 128 B maps every row to the same banks)
+template <int N, bool SWZ>
+__device__ __forceinline__ int uidx(int c, int R) {
+  if constexpr (SWZ)
+    return R * 16 + ((((c >> 1) ^ (R & 7)) << 1) | (c & 1));
+  else
+    return c + N * R;
+}
+
+template <int N, int G, int SGS, int KS, bool SUMSQ, bool SWZ = false>
 __global__ void __launch_bounds__(G *TcCfg<N>::T, 1)
     semlap_tc2_kernel(double *__restrict__ w, const double *__restrict__ u,
                       const double *__restrict__ g, int64_t nelt,
-                      double *__restrict__ partials) {
+                      double *__restrict__ partials,
+                      const __grid_constant__ CUtensorMap umap) {
   using C = TcCfg<N>;
-  using L = Tc2Smem<N, G, SGS, KS>;
+  using L = Tc2Smem<N, G, SGS, KS, SWZ>;
   constexpr int NP = C::NP, T = C::T, KT = C::KT, P = C::P, SL = C::SL;
   constexpr int N2 = N * N;
   static_assert(N >= 7 && N <= 16, "n = 7..16");
   static_assert(N % KS == 0, "KS divides n");
   static_assert(G * (1 + SGS) <= 64 && G <= 15, "mbarriers, barrier ids");
+  static_assert(!SWZ || N == 16, "swizzled staging: 128-B rows (n = 16)");
 
-  extern __shared__ __align__(128) unsigned char smem[];
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char *smem = smem_raw;
+  if constexpr (SWZ) {  // the swizzle pattern is of the absolute address
+    const uint32_t a = smem_u32(smem_raw);
+    smem += ((a + 1023u) & ~1023u) - a;
+  }
   uint64_t *bars = reinterpret_cast<uint64_t *>(smem);
 
   const int tid = threadIdx.x;
@@ -415,6 +441,16 @@ __global__ void __launch_bounds__(G *TcCfg<N>::T, 1)
   };
   auto issue_u = [&](int64_t m) {
     const int64_t e = elem(m);
+    if constexpr (SWZ) {  // rows e N^2 .. e N^2 + N^2 - 1 of the (16 x rows) map
+      mbar_arrive_expect_tx(ubar, (uint32_t)(NP * 8));
+      asm volatile(
+          "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::"
+          "complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+              smem_u32(ust0)),
+          "l"(&umap), "r"(0), "r"((int)(e * N2)), "r"(smem_u32(ubar))
+          : "memory");
+      return;
+    }
     if (u_bulk_ok(e)) {
       mbar_arrive_expect_tx(ubar, (uint32_t)u_span(e));
       bulk_g2s_stream(ust0, u + e * NP - u_lead(e), (uint32_t)u_span(e),
@@ -451,8 +487,8 @@ __global__ void __launch_bounds__(G *TcCfg<N>::T, 1)
   for (int64_t m = 0; m < mine; ++m) {
     const int64_t e = elem(m);
     mbar_wait(ubar, (uint32_t)(m & 1));
-    const double *ust = ust0 + u_lead(e);
-    if (!u_bulk_ok(e)) {
+    const double *ust = SWZ ? ust0 : ust0 + u_lead(e);
+    if (!SWZ && !u_bulk_ok(e)) {
       for (int x = lt; x < NP; x += T) ust0[u_lead(e) + x] = u[e * NP + x];
       named_bar_sync(1 + grp, T);
     }
@@ -462,8 +498,8 @@ __global__ void __launch_bounds__(G *TcCfg<N>::T, 1)
       double uc0[N], uc1[N];
 #pragma unroll
       for (int l = 0; l < N; ++l) {
-        uc0[l] = v0 ? ust[i0 + N * j + N2 * l] : 0.0;
-        uc1[l] = v1 ? ust[i0 + 1 + N * j + N2 * l] : 0.0;
+        uc0[l] = v0 ? ust[uidx<N, SWZ>(i0, j + N * l)] : 0.0;
+        uc1[l] = v1 ? ust[uidx<N, SWZ>(i0 + 1, j + N * l)] : 0.0;
       }
 #pragma unroll
       for (int k = 0; k < N; ++k) t0[k] = t1[k] = 0.0;
@@ -486,10 +522,10 @@ __global__ void __launch_bounds__(G *TcCfg<N>::T, 1)
       double r0 = 0.0, r1 = 0.0, s0 = 0.0, s1 = 0.0;
 #pragma unroll
       for (int ks = 0; ks < KT; ++ks) {
-        dmma(r0, r1, ust[(4 * ks + q) + N * (8 * jt + r) + N2 * k],
+        dmma(r0, r1, ust[uidx<N, SWZ>(4 * ks + q, 8 * jt + r + N * k)],
              fa_r[ks]);
         dmma(s0, s1, fb_s[ks],
-             ust[(8 * it + r) + N * (4 * ks + q) + N2 * k]);
+             ust[uidx<N, SWZ>(8 * it + r, 4 * ks + q + N * k)]);
       }
       if (k % KS == 0)
         mbar_wait(&gbar[(s / KS) % SGS], (uint32_t)((s / KS / SGS) & 1));
@@ -531,15 +567,17 @@ __global__ void __launch_bounds__(G *TcCfg<N>::T, 1)
         fence_proxy_async_smem();
         issue_u(m + 1);  // u consumed by every warp (barrier above)
       }
-      // ---- phase 2 sums over wr / ws of slice k (tensor cores)
-      double a0 = 0.0, a1 = 0.0;
+      // ---- phase 2 sums over wr / ws of slice k (tensor cores): two
+      // independent accumulator chains (d^T.wr and ws.d), added at the end,
+      // so the DMMA latency is paid over KT steps, not 2 KT
+      double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
 #pragma unroll
       for (int ks = 0; ks < KT; ++ks) {
         dmma(a0, a1, wr_k[(4 * ks + q) + P * (8 * jt + r)], fa_t[ks]);
-        dmma(a0, a1, fb_t[ks], ws_k[(8 * it + r) + P * (4 * ks + q)]);
+        dmma(b0, b1, fb_t[ks], ws_k[(8 * it + r) + P * (4 * ks + q)]);
       }
-      p0[k] = a0;
-      p1[k] = a1;
+      p0[k] = a0 + b0;
+      p1[k] = a1 + b1;
     }
     // ---- the own-column sum over wt (needs every slice), then w
     double *we = w + e * NP;
@@ -571,12 +609,37 @@ __global__ void __launch_bounds__(G *TcCfg<N>::T, 1)
   if constexpr (SUMSQ) block_sumsq_partial(acc_sq, partials);
 }
 
+// the (16 x rows) view of u for the swizzled staging (n = 16)
+static bool make_u_map(CUtensorMap *map, const double *u, int64_t nelt) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    return (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p,
+                                    cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+               ? reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p)
+               : nullptr;
+  }();
+  if (!encode || !aligned(u, 16) || nelt * 256 >= (int64_t(1) << 31))
+    return false;
+  cuuint64_t dims[2] = {16, (cuuint64_t)(nelt * 256)};
+  cuuint64_t strides[1] = {128};
+  cuuint32_t box[2] = {16, 256};
+  cuuint32_t estr[2] = {1, 1};
+  return encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2,
+                const_cast<double *>(u), dims, strides, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <int N, int G, int SGS, int KS>
 static int launch_tc2(double *w, const double *u, const double *d,
                       const double *g, int64_t nelt, const lfb_launch *geom,
                       cudaStream_t s, int64_t *grid_out) {
   using L = Tc2Smem<N, G, SGS, KS>;
-  static_assert(L::total <= 227 * 1024, "smem");
+  using LS = Tc2Smem<N, G, SGS, KS, N == 16>;
+  static_assert(L::total <= 227 * 1024 && LS::total <= 227 * 1024, "smem");
   int sms = sm_count(geom);
   if (sms <= 0) sms = 148;
   const int per_sm = (geom && geom->ctas_per_sm > 0) ? geom->ctas_per_sm : 1;
@@ -590,10 +653,20 @@ static int launch_tc2(double *w, const double *u, const double *d,
   const bool sumsq = geom && geom->sumsq;
   if (sumsq && (!geom->workspace || geom->workspace_len < grid))
     return fail(LFB_ERR_ARG, "semlap: sumsq workspace too small");
+  // n = 16: swizzled u staging when the tensor map encodes (geom->variant
+  // 54 forces the plain staging, for the tests)
+  alignas(64) CUtensorMap umap;
+  memset(&umap, 0, sizeof(umap));
+  const bool swz = N == 16 && !(geom && geom->variant == 54) &&
+                   make_u_map(&umap, u, nelt);
   auto k = sumsq ? semlap_tc2_kernel<N, G, SGS, KS, true>
                  : semlap_tc2_kernel<N, G, SGS, KS, false>;
-  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)L::total);
+  auto ks = sumsq ? semlap_tc2_kernel<N, G, SGS, KS, true, N == 16>
+                  : semlap_tc2_kernel<N, G, SGS, KS, false, N == 16>;
+  const size_t bytes = swz ? LS::total : L::total;
+  cudaFuncSetAttribute(swz ? ks : k,
+                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)bytes);
   {
     std::unique_lock<std::mutex> lk;
     bool capturing = false;
@@ -601,8 +674,8 @@ static int launch_tc2(double *w, const double *u, const double *d,
     if (int rc = dconst_acquire(c_dtc, 256 * 8, 3, &slot, d, N, s, &lk,
                                 &capturing))
       return rc;
-    k<<<grid, G * TcCfg<N>::T, L::total, s>>>(
-        w, u, g, nelt, sumsq ? geom->workspace : nullptr);
+    (swz ? ks : k)<<<grid, G * TcCfg<N>::T, bytes, s>>>(
+        w, u, g, nelt, sumsq ? geom->workspace : nullptr, umap);
     dconst_release(3, slot, s, capturing);
   }
   if (int rc = check_launch("lfb_semlap_f64(dmma2)")) return rc;
@@ -680,6 +753,7 @@ static int launch_tc(double *w, const double *u, const double *d,
   X(14, 52, 3, 2, 1)     \
   X(15, 52, 3, 2, 1)     \
   X(16, 52, 2, 4, 1)     \
+  X(16, 54, 2, 4, 1)     \
   X(12, 53, 2, 3, 2)     \
   X(13, 53, 2, 3, 1)     \
   X(14, 53, 2, 3, 1)     \

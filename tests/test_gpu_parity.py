@@ -174,10 +174,13 @@ def test_semlap_ragged_and_guarded(cuda, block, nelt):
                          + [(n, 51) for n in range(9, 17)]
                          + [(n, 61) for n in (7, 9, 10, 11, 12)]
                          + [(n, 52) for n in range(7, 17)] + [(8, 53),
-                                                              (8, 55)])
+                                                              (8, 55),
+                                                              (16, 54)])
 def test_semlap_fma_mode(cuda, n, variant):
     """variant 50: the default kernel with every multiply-add fused (DFMA);
-    variant 51: the FP64 tensor-core (DMMA) kernel for even n >= 10.
+    variant 51: the FP64 tensor-core (DMMA) kernel for even n >= 10;
+    52: the interleaved-phase DMMA kernel (n = 16: u staged by a swizzled
+    2-D TMA), 54: the same with the plain bulk-copy staging.
     Tolerance parity (north star: 1e-12 relative fp64): per point against
     the magnitude of the terms it sums -- the same operator on |u|, |d|,
     |g| -- and normwise."""
