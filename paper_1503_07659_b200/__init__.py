@@ -21,8 +21,8 @@ See DESIGN.md for the kernels and INTEGRATION.md for the ABI bindings.
 from .cudagen import emit_cuda
 from .executor import (ENGINES, DeviceArray, DeviceEnv, Launcher,
                        env_from_buffers, flat_outputs, get_device_output,
-                       get_output, interpret, make_device_env, make_launcher,
-                       plan_for)
+                       get_output, interpret, interpret_bounds_checked,
+                       make_device_env, make_launcher, plan_for)
 from .launch import Geometry, launch_geometry
 from .recognize import WORKLOADS, canonicalize, recognize
 
@@ -30,6 +30,7 @@ __all__ = [
     "ENGINES", "emit_cuda", "make_launcher",
     "DeviceArray", "DeviceEnv", "Launcher", "env_from_buffers",
     "flat_outputs", "get_device_output", "get_output", "interpret",
+    "interpret_bounds_checked",
     "make_device_env", "plan_for", "Geometry", "launch_geometry",
     "WORKLOADS", "canonicalize", "recognize",
 ]

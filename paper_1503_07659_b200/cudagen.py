@@ -74,6 +74,21 @@ template <typename T> static __device__ __forceinline__ T lfb_npmax(T a, T b) {
 }
 """
 
+CHECK_PRELUDE = r"""
+/* checked execution: the first out-of-bounds access of the launch is
+   recorded -- [flag, insn, array, mode, rank, idx0..4, ext0..4] -- and the
+   access skipped (loads read 0); the host raises InterpError */
+static __device__ __noinline__ void lfb_oob(long long *err, int insn, int arr,
+    int mode, int rank, i64 i0, i64 i1, i64 i2, i64 i3, i64 i4,
+    i64 x0, i64 x1, i64 x2, i64 x3, i64 x4) {
+  if (atomicCAS((unsigned long long *)err, 0ull, 1ull) != 0ull) return;
+  err[1] = insn; err[2] = arr; err[3] = mode; err[4] = rank;
+  err[5] = i0; err[6] = i1; err[7] = i2; err[8] = i3; err[9] = i4;
+  err[10] = x0; err[11] = x1; err[12] = x2; err[13] = x3; err[14] = x4;
+  __threadfence();
+}
+"""
+
 TMA_PRELUDE = r"""
 /* precompute footprints by TMA (SURVEY.md §8(f) row 3) */
 struct __align__(64) lfb_tmap { unsigned long long v[16]; };
@@ -221,13 +236,25 @@ class Program:
     cooperative: int        # fetch nests distributed over the CTA
     key: str                # content hash of the source
     tma: tuple = ()         # tensor maps (TmaMap), kernel params after lfb_G*
+    checked: str = None     # None, "plain" or "dims"
+    insn_ids: tuple = ()    # checked mode: instruction ids by index
+    arr_names: tuple = ()   # checked mode: array names by index
 
 
 class _Emitter:
-    def __init__(self, kernel):
+    def __init__(self, kernel, checked=None):
         k = transforms.expand_all_rules(kernel) if kernel.rules else kernel
         lfk.validate_kernel(k)
         self.k = k
+        # checked=None: the fast kernel.  "plain" / "dims": every array
+        # access checked like the reference's _Evaluator.check_bounds
+        # (interp.py:293-308) -- arguments per dimension against the env's
+        # shapes, temporaries by flat offset ("plain", interpret()) or per
+        # dimension ("dims", interpret_bounds_checked) -- the first
+        # violation recorded for the host to raise; no layout tricks then
+        self.checked = checked
+        self.cur_insn = None
+        self.insn_ids = [insn.id for insn in k.instructions]
         self.imap = k.instruction_map()
         self.tree = codegen.group_predicates(codegen.schedule(k))
         self.parallel = codegen.parallel_inames_of(k)
@@ -246,7 +273,7 @@ class _Emitter:
                 self.scalars.add(a.name)
         self.temp_shapes = {}
         self.temp_alloc = {}
-        self.tma_plan = self._plan_tma(k)
+        self.tma_plan = {} if checked else self._plan_tma(k)
         self.tma_maps = []     # TmaMap per emitted footprint
         self.tma_index = {}    # temp -> map index
         self.pipes = 0         # double-buffered (prefetching) loops
@@ -266,7 +293,8 @@ class _Emitter:
                 self.temp_shapes[t.name] = tuple(shape)
                 alloc = list(shape)
                 if t.address_space == "workgroup" and len(shape) >= 2 \
-                        and shape[-1] % 2 == 0 and t.name not in self.tma_plan:
+                        and shape[-1] % 2 == 0 and t.name not in \
+                        self.tma_plan and not checked:
                     # odd row pitch: work-items reading down a column of a
                     # shared tile hit distinct banks (the layout of a
                     # temporary is the executor's choice, interp.py:408-414)
@@ -282,6 +310,8 @@ class _Emitter:
         self.visible = list(self.parallel)
         self.tmp = 0
         self.cooperative = 0
+        self.arr_names = []   # checked mode: array ids in error records
+        self.ext_args = set()  # checked mode: arguments needing extents
         self.promoted = {}    # array -> (subscript, register name)
         self.n_promoted = 0
         self.written = set()
@@ -314,6 +344,11 @@ class _Emitter:
             hit = self.promoted.get(e.array)
             if hit is not None and hit[0] == e:
                 return hit[1], self.dtypes[e.array]
+            if self.checked:
+                cond, rec = self._bounds(e)
+                z = _lit_int(0, self.dtypes[e.array])
+                return (f"(({cond}) ? {e.array}[{self.flat(e)}] : "
+                        f"({rec}, {z}))", self.dtypes[e.array])
             return f"{e.array}[{self.flat(e)}]", self.dtypes[e.array]
         if isinstance(e, ex.Compare):
             lt_, lt = self.rv(e.left)
@@ -605,16 +640,28 @@ class _Emitter:
             self.ind += 1
         tgt = insn.lhs.name if isinstance(insn.lhs, ex.VarRef) \
             else insn.lhs.array
+        self.cur_insn = self.insn_ids.index(insn.id)
         rhs, rt = self.rv(insn.rhs)
         hit = self.promoted.get(tgt)
+        store_if = None
         if isinstance(insn.lhs, ex.VarRef):
             lhs = insn.lhs.name
         elif hit is not None and hit[0] == insn.lhs:
             lhs = hit[1]
         else:
             lhs = f"{insn.lhs.array}[{self.flat(insn.lhs)}]"
-        self.line(f"{lhs} = {_cast(rhs, rt, self.dtypes[tgt])};  "
-                  f"/* {insn.id} */")
+            if self.checked:
+                store_if = self._bounds(insn.lhs)
+        val = _cast(rhs, rt, self.dtypes[tgt])
+        if store_if is not None:
+            # the value first (its loads are checked before the store, the
+            # reference's evaluation order), then the checked store
+            cond, rec = store_if
+            ct = CT[self.dtypes[tgt]]
+            self.line(f"{{ const {ct} lfb_v = {val}; if ({cond}) {lhs} = "
+                      f"lfb_v; else {rec}; }}  /* {insn.id} */")
+        else:
+            self.line(f"{lhs} = {val};  /* {insn.id} */")
         if guarded:
             self.ind -= 1
             self.line("}")
@@ -961,6 +1008,8 @@ class _Emitter:
         reference would not make), and every access to the array inside the
         loop must use that one subscript (arguments never alias: each is its
         own buffer)."""
+        if self.checked:
+            return []
         direct = [self.imap[c.insn_id] for c in node.children
                   if isinstance(c, codegen.Statement)]
         cands = {}
@@ -1073,6 +1122,46 @@ class _Emitter:
         if sum(1 for _ in self._stmts(node)) > 4:
             return None
         return lo, hi
+
+    def _bounds(self, e):
+        """(in-bounds condition, failure record) of subscript *e*."""
+        idx = []
+        for ix in e.index:
+            aff = ex.expression_to_affine(ix)
+            if aff is not None:
+                idx.append(f"(i64)({_aff(aff)})")
+            else:
+                txt, _t = self.rv(ix)
+                idx.append(f"(i64)({txt})")
+        names = self.arr_names
+        if e.array not in names:
+            names.append(e.array)
+        a = names.index(e.array)
+        insn = self.cur_insn if self.cur_insn is not None else -1
+        if e.array in self.temp_shapes:
+            shape = self.temp_shapes[e.array]
+            if self.checked == "dims":
+                ext = [str(n) for n in shape]
+            else:  # the flat offset against the dense temporary
+                size = 1
+                for n in shape:
+                    size *= n
+                flat = self.flat(e)
+                return (f"(unsigned long long)(i64)({flat}) < {size}ull",
+                        f"lfb_oob(lfb_err, {insn}, {a}, -1, {len(idx)}, "
+                        + ", ".join(idx + ["0"] * (5 - len(idx)))
+                        + ", 0, 0, 0, 0, 0)")
+        else:
+            ext = [f"lfb_x_{e.array}_{d}" for d in range(len(idx))]
+            self.ext_args.add(e.array)
+        cond = " && ".join(f"(unsigned long long)({i}) < "
+                           f"(unsigned long long)({x})"
+                           for i, x in zip(idx, ext)) or "true"
+        pad = ["0"] * (5 - len(idx))
+        rec = (f"lfb_oob(lfb_err, {insn}, {a}, 0, {len(idx)}, "
+               + ", ".join(idx + pad) + ", "
+               + ", ".join([f"(i64)({x})" for x in ext] + pad) + ")")
+        return cond, rec
 
     def _touches(self, node, wg):
         w = r = False
@@ -1391,6 +1480,14 @@ class _Emitter:
             sig.append(f"i64 lfb_G{a}")
             order.append(f"lfb_G{a}")
         prelude = PRELUDE
+        if self.checked:
+            prelude += CHECK_PRELUDE
+            sig.append("long long *lfb_err")
+            order.append("lfb_err")
+            for name in sorted(self.ext_args):
+                for d in range(len(self.arrays[name])):
+                    sig.append(f"i64 lfb_x_{name}_{d}")
+                    order.append(f"lfb_x_{name}_{d}")
         if self.tma_maps:
             sig.append("int lfb_tma")
             order.append("lfb_tma")
@@ -1425,13 +1522,16 @@ class _Emitter:
         key = hashlib.sha256(src.encode()).hexdigest()[:16]
         return Program(src, entry, tuple(order), params, tuple(block),
                        tuple(sorted(shared)), tuple(sorted(demoted)),
-                       self.cooperative, key, tuple(self.tma_maps))
+                       self.cooperative, key, tuple(self.tma_maps),
+                       self.checked, tuple(self.insn_ids),
+                       tuple(self.arr_names))
 
 
-def emit_cuda(kernel):
+def emit_cuda(kernel, checked=None):
     """Render *kernel* (transformed, rules expanded or not) as one CUDA
-    kernel; returns a :class:`Program`."""
-    return _Emitter(kernel).emit()
+    kernel; returns a :class:`Program`.  *checked*: None, "plain" (the
+    reference's interpret() checks) or "dims" (interpret_bounds_checked)."""
+    return _Emitter(kernel, checked).emit()
 
 
 __all__ = ["Program", "TmaMap", "emit_cuda", "NVRTC_OPTIONS", "promote"]

@@ -83,7 +83,8 @@ def _device(device):
     return torch.device(device)
 
 
-def make_device_env(kernel, params, inputs=None, seed=None, device=None):
+def make_device_env(kernel, params, inputs=None, seed=None, trace=False,
+                    device=None):
     """Bind parameters and device arrays for a kernel run (interp.py:79-123).
 
     *inputs* maps argument names to numpy arrays / torch tensors of logical
@@ -93,6 +94,13 @@ def make_device_env(kernel, params, inputs=None, seed=None, device=None):
     argument order), so a seeded device env holds exactly the values of the
     seeded reference env.
     """
+    if trace:
+        # interp.py:79/381-382 appends (insn, array, index) per write in the
+        # sequential interpreter's order; device work-items write in
+        # parallel, so there is no such order to record
+        raise InterpError("make_env(trace=True) is the sequential "
+                          "interpreter's write trace; the device executor "
+                          "has none (run loopforge.interp for it)")
     dev = _device(device)
     inputs = dict(inputs or {})
     params = {k: int(v) for k, v in params.items()}
@@ -301,23 +309,75 @@ def make_launcher(kernel, env, variant=0, engine="auto"):
                                "(no CPU fallback)") from exc2
 
 
-def interpret(kernel, env, inplace=False, variant=0, stream=None,
-              engine="auto"):
-    """Run *kernel* on the B200 (drop-in for interp.py:323).
+def _never_written(kernel):
+    """interp.py:272-291 raises on a read of a temporary no instruction
+    wrote; here the same condition is found before the launch: a
+    temporary read by some instruction and written by none."""
+    from ._loopforge import ex, transforms
+    k = transforms.expand_all_rules(kernel) if kernel.rules else kernel
+    written = set()
+    for insn in k.instructions:
+        lhs = insn.lhs
+        written.add(lhs.array if isinstance(lhs, ex.Subscript) else lhs.name)
+    for insn in k.instructions:
+        for e in insn.read_expressions():
+            for name in ex.free_variables(e):
+                if name in k.temporaries and name not in written:
+                    raise InterpError(f"read of never-written temporary "
+                                      f"'{name}' in {insn.id}")
+
+
+def _shapes_as_declared(kernel, env):
+    for a in kernel.args:
+        if a.kind != "global-array":
+            continue
+        want = tuple(s.eval(env.params) for s in a.shape)
+        if tuple(env.arrays[a.name].shape) != want:
+            return False
+    return True
+
+
+def interpret(kernel, env, bounds_check=False, *, inplace=False, variant=0,
+              stream=None, engine="auto"):
+    """Run *kernel* on the B200 (drop-in for interp.py:323, same
+    ``interpret(kernel, env, bounds_check=False)`` signature).
 
     Returns a new :class:`DeviceEnv` whose output arrays hold the results;
     the launch is asynchronous on the current CUDA stream (or *stream*).
+
+    ``bounds_check=True`` (``interpret_bounds_checked``, interp.py:403) runs
+    the checked build of the generated CUDA: every argument subscript
+    checked per dimension against the env's shapes and every temporary
+    subscript per dimension; the first violation raises the reference's
+    InterpError naming the instruction.  The same checked build (temporaries
+    by flat offset, the reference's plain mode) runs when an env's array
+    shapes no longer match the kernel's declarations -- the case in which
+    the reference's always-on argument checks can fire.  Otherwise the
+    recognised hand-written kernel runs unchecked.
     """
     check_assumptions(kernel, env.params)
+    _never_written(kernel)
     out = DeviceEnv(dict(env.params), dict(env.arrays), dict(env.scalars),
                     env.device)
     if not inplace:
         for a in kernel.args:
             if a.kind == "global-array" and a.is_output:
                 out.arrays[a.name] = env.arrays[a.name].copy()
-    make_launcher(kernel, out, variant=variant, engine=engine).launch(
-        stream=stream)
+    if bounds_check or not _shapes_as_declared(kernel, env):
+        from .generic import GenericLauncher
+        launcher = GenericLauncher(kernel, out,
+                                   checked="dims" if bounds_check
+                                   else "plain")
+    else:
+        launcher = make_launcher(kernel, out, variant=variant, engine=engine)
+    launcher.launch(stream=stream)
     return out
+
+
+def interpret_bounds_checked(kernel, env, **kw):
+    """As :func:`interpret`, with every temporary access checked per
+    dimension (interp.py:403-405)."""
+    return interpret(kernel, env, bounds_check=True, **kw)
 
 
 def get_device_output(env, name):

@@ -14,6 +14,7 @@ import ctypes as C
 import torch
 
 from . import abi
+from ._loopforge import InterpError
 from .cudagen import NVRTC_OPTIONS, emit_cuda
 from .launch import launch_geometry
 
@@ -22,14 +23,14 @@ _MODULES = {}   # (program key, device index) -> lfb_module handle
 _PROGRAMS = {}  # id(kernel) -> (kernel, Program)
 
 
-def program_for(kernel):
-    hit = _PROGRAMS.get(id(kernel))
+def program_for(kernel, checked=None):
+    hit = _PROGRAMS.get((id(kernel), checked))
     if hit is not None and hit[0] is kernel:
         return hit[1]
-    prog = emit_cuda(kernel)
+    prog = emit_cuda(kernel, checked=checked)
     if len(_PROGRAMS) > 256:
         _PROGRAMS.clear()
-    _PROGRAMS[id(kernel)] = (kernel, prog)
+    _PROGRAMS[(id(kernel), checked)] = (kernel, prog)
     return prog
 
 
@@ -89,10 +90,10 @@ class GenericLauncher:
     """Prepared launch of the generated kernel (same interface as
     executor.Launcher)."""
 
-    def __init__(self, kernel, env):
+    def __init__(self, kernel, env, checked=None):
         self.kernel = kernel
         self.env = env
-        self.program = program_for(kernel)
+        self.program = program_for(kernel, checked)
         self.geometry = launch_geometry(kernel, env.params)
         self._narrow = {}
 
@@ -172,6 +173,12 @@ class GenericLauncher:
                 vals.append(C.c_int64(gext[int(name[5:])]))
             elif name == "lfb_tma":
                 vals.append(C.c_int32(1 if tma_ok else 0))
+            elif name == "lfb_err":
+                err = torch.zeros(16, dtype=torch.int64, device=dev)
+                vals.append(C.c_void_p(err.data_ptr()))
+            elif name.startswith("lfb_x_"):   # checked mode: env extents
+                arr, d = name[6:].rsplit("_", 1)
+                vals.append(C.c_int64(int(env.arrays[arr].shape[int(d)])))
             elif name.startswith("lfb_tm"):
                 vals.append(maps[int(name[6:])])
             elif a is None:                    # a parameter (int64)
@@ -192,6 +199,31 @@ class GenericLauncher:
         abi.check(abi.load().lfb_module_launch(mod, grid, block, 0, argv,
                                                stream),
                   f"launch {prog.entry}")
+        if prog.checked:
+            self._raise_first_oob(err, env)
+
+    def _raise_first_oob(self, err, env):
+        """The reference's InterpError for the recorded access
+        (interp.py:293-308 check_bounds messages)."""
+        rec = err.cpu().tolist()     # synchronises: a debugging mode
+        if not rec[0]:
+            return
+        prog = self.program
+        insn = prog.insn_ids[rec[1]] if rec[1] >= 0 else None
+        name = prog.arr_names[rec[2]]
+        rank = rec[4]
+        idx = tuple(rec[5:5 + rank])
+        if rec[3] == -1:          # temporary, flat offset (plain mode)
+            raise InterpError(f"out-of-bounds subscript {idx} of '{name}' "
+                              f"in instruction {insn}")
+        if name in env.arrays:
+            shape = tuple(int(x) for x in env.arrays[name].shape)
+        else:
+            shape = tuple(rec[10:10 + rank])
+        d = next((i for i, (v, n) in enumerate(zip(idx, shape))
+                  if not 0 <= v < n), 0)
+        raise InterpError(f"out-of-bounds subscript {idx} of '{name}' "
+                          f"(extent {shape}) in instruction {insn}, dim {d}")
 
 
 __all__ = ["GenericLauncher", "program_for", "compile_program"]

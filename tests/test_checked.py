@@ -1,0 +1,130 @@
+"""The reference's run-time checks, on the device (race
+detection / sanitizers; the reference's tests/test_interp.py:139-192).
+
+* ``interpret(kernel, env, bounds_check=False)`` keeps the reference's
+  signature (interp.py:323); ``interpret_bounds_checked`` (403-405) exists.
+* Out-of-bounds subscripts raise InterpError naming the instruction: the
+  checked build of the generated CUDA records the first violation of a
+  launch (cudagen.py ``checked``), the host raises the reference's message.
+* A read of a temporary no instruction writes raises "never-written".
+* ``make_env(trace=True)``'s sequential write trace has no device analogue:
+  a clear InterpError, not a silently missing attribute.
+"""
+
+import dataclasses
+import inspect
+
+import numpy as np
+import pytest
+import torch
+
+import paper_1503_07659_b200 as lfb
+from conftest import Golden
+from paper_1503_07659_b200 import fixtures as fx
+from paper_1503_07659_b200._loopforge import (InterpError, kernel as lfk,
+                                              polyset, transforms)
+from paper_1503_07659_b200.cudagen import emit_cuda
+from paper_1503_07659_b200.generic import compile_program
+
+
+def sec51_precomputed():
+    """The reference's §5.1 forward difference with a precomputed tile
+    (tests/test_interp.py sec51_precomputed)."""
+    knl = lfk.make_kernel(["{[i]: 0<=i<n}"], "result[i] = u[i+1]-u[i]",
+                          name="fwd_diff")
+    knl = transforms.split_iname(knl, "i", 16)
+    knl = transforms.assume(knl, "n mod 16 = 0")
+    knl = transforms.extract_subst(knl, "u_acc", "u[j]", parameters="j")
+    return transforms.precompute(knl, "u_acc", "i_inner", default_tag=None)
+
+
+def test_interpret_keeps_the_reference_signature():
+    params = list(inspect.signature(lfb.interpret).parameters)
+    assert params[:3] == ["kernel", "env", "bounds_check"]
+    assert callable(lfb.interpret_bounds_checked)
+
+
+def test_read_never_written_temporary():
+    knl = lfk.make_kernel(["{[i]: 0<=i<4}"], "<> t = a[i]\nout[i] = t")
+    reader = dataclasses.replace(knl.instructions[1],
+                                 depends_on=frozenset())
+    broken = knl.copy(instructions=(reader,))
+    env = lfb.make_device_env(broken, {}, {"a": np.ones(4, np.float32)},
+                              device="cpu")
+    with pytest.raises(InterpError, match="never-written"):
+        lfb.interpret(broken, env)
+
+
+def test_trace_has_no_device_analogue():
+    knl = lfk.make_kernel(["{[i]: 0<=i<n}"], "out[i] = 2*a[i]")
+    with pytest.raises(InterpError, match="trace"):
+        lfb.make_device_env(knl, {"n": 4}, trace=True, device="cpu")
+
+
+@pytest.mark.parametrize("mode", ["plain", "dims"])
+def test_checked_builds_compile(mode):
+    for src in (fx.gemm_source("f64"), fx.generic_source("matvec_acc"),
+                fx.semlap_source(4, block=2)):
+        _raw, knl = fx.translate(src)
+        prog = emit_cuda(knl, checked=mode)
+        assert prog.checked == mode and "lfb_oob(" in prog.source
+        assert not prog.tma                 # plain layouts when checked
+        assert compile_program(prog, True)[:4] == b"\x7fELF"
+
+
+@pytest.mark.gpu
+def test_out_of_bounds_reports_instruction(cuda):
+    """tests/test_interp.py:139-147: the env lies about a's extent."""
+    knl = lfk.make_kernel(["{[i]: 0<=i<n}"], "out[i] = a[i+3]")
+    env = lfb.make_device_env(knl, {"n": 6},
+                              {"a": np.ones(9, dtype=np.float32)},
+                              device=cuda)
+    env.arrays["a"].shape = (4,)
+    with pytest.raises(InterpError, match="insn_0"):
+        lfb.interpret(knl, env)
+
+
+@pytest.mark.gpu
+def test_bounds_checked_forward_diff_ok(cuda):
+    knl = sec51_precomputed()
+    u = np.random.default_rng(11).random(33).astype(np.float32)
+    env = lfb.make_device_env(knl, {"n": 32}, {"u": u}, device=cuda)
+    out = lfb.interpret_bounds_checked(knl, env)
+    want = u[1:] - u[:-1]
+    assert np.array_equal(lfb.get_output(out, "result"), want)
+
+
+@pytest.mark.gpu
+def test_bounds_checked_detects_shrunk_temp(cuda):
+    knl = sec51_precomputed()
+    temp = knl.temporaries["u_acc_0"]
+    shrunk = lfk.TemporaryDecl(temp.name, temp.dtype,
+                               (polyset.AffineExpr.const(16),),
+                               temp.address_space, temp.base_offsets)
+    bad = knl.copy(temporaries={**knl.temporaries, "u_acc_0": shrunk})
+    env = lfb.make_device_env(bad, {"n": 32},
+                              {"u": np.ones(33, dtype=np.float32)},
+                              device=cuda)
+    with pytest.raises(InterpError, match="u_acc_0"):
+        lfb.interpret_bounds_checked(bad, env)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["gen_dgemm_m20_n12_l40", "gen_mvacc_n64",
+                                  "gen_stencil_n250", "gen_rowsum_n40_m17",
+                                  "semlap_n5_b2_nelt2"])
+def test_bounds_checked_same_results(name, cuda):
+    """In-bounds kernels: the checked build gives the reference's bits."""
+    g = Golden(name)
+    _raw, knl = g.kernels()
+    env = lfb.make_device_env(knl, g.params, device=cuda)
+    for a in knl.args:
+        buf = g.inp(a.name)
+        if a.kind == "scalar-value":
+            env.scalars[a.name] = buf.reshape(-1)[0]
+        else:
+            env.arrays[a.name].data.copy_(torch.from_numpy(buf.copy()))
+    out = lfb.interpret_bounds_checked(knl, env)
+    for o in g.outputs():
+        assert out.arrays[o].data.cpu().numpy().tobytes() == \
+            g.out(o).tobytes(), f"{name}:{o}"
