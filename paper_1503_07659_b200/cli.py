@@ -9,7 +9,7 @@ An input file holds either the logical array or, 1-D, the flat strided
 buffer (interp.py FlatArray.data / the emitted C's arrays).
     python -m paper_1503_07659_b200 translate <file.f> --target c|opencl|cuda
     python -m paper_1503_07659_b200 dump-ir <file.f> --stage raw|transformed|expanded
-    python -m paper_1503_07659_b200 check <file.f> [--param n=32]
+    python -m paper_1503_07659_b200 check <file.f> [--param n=32 [--smoke]]
 
 ``--transforms <script>`` (any mode) applies an extra transform script after
 the embedded ``!$loopy`` blocks, in that order.  Array
@@ -102,13 +102,54 @@ def cmd_check(args):
         report["cuda_entry"] = prog.entry
         report["block"] = list(prog.block)
     params = _kv(args.param, "--param", int)
+    rc = 0
     if params:
         g = launch_geometry(knl, params)
         report["launch"] = {"group_extent": list(g.group_extent),
                             "local_extent": list(g.local_extent),
                             "guard": bool(g.guard)}
+        if args.smoke:
+            report["smoke"] = _engine_smoke(knl, params, args)
+            rc = 0 if report["smoke"]["agree"] else 1
     print(json.dumps(report))
-    return 0
+    return rc
+
+
+def _engine_smoke(knl, params, args):
+    """The check mode's property smoke test (SPEC.md cli: "validate +
+    property smoke tests"): the same seeded inputs through the hand-written
+    kernel (when recognised) and the generated CUDA, both on the device;
+    their outputs must agree -- bitwise where both keep the reference's
+    arithmetic, within the north star's tolerance where the default kernel
+    reassociates (matvec split-j, tensor-core GEMM)."""
+    import numpy as np
+    import torch
+
+    from ._loopforge import InterpError
+    from .executor import interpret, make_device_env
+    if not torch.cuda.is_available():
+        raise InterpError("check --smoke runs on the B200: no CUDA device")
+    dev = torch.device("cuda", args.device)
+    env = make_device_env(knl, params, seed=args.seed or 0, device=dev)
+    outs = [a.name for a in knl.args
+            if a.kind == "global-array" and a.is_output]
+    res = {}
+    for engine in ("auto", "generic"):
+        o = interpret(knl, env, engine=engine)
+        res[engine] = {n: o.arrays[n].data.cpu().numpy() for n in outs}
+    worst, bitwise = 0.0, True
+    for n in outs:
+        x, y = res["auto"][n], res["generic"][n]
+        bitwise &= x.tobytes() == y.tobytes()
+        if x.size and np.issubdtype(x.dtype, np.floating):
+            scale = float(np.max(np.abs(y))) or 1.0
+            worst = max(worst, float(np.max(np.abs(x - y))) / scale)
+        elif x.tobytes() != y.tobytes():
+            worst = float("inf")
+    tol = 1e-5 if any(a.dtype == "f32" for a in knl.args) else 1e-12
+    return {"outputs": outs, "bitwise": bitwise,
+            "max_rel_diff": worst, "tolerance": tol,
+            "agree": bitwise or worst <= tol}
 
 
 def cmd_run(args):
@@ -154,7 +195,8 @@ def cmd_run(args):
     for name, t in flat.items():
         env.arrays[name].data.copy_(t)
     t0 = time.perf_counter()
-    out = interpret(knl, env, variant=args.variant, engine=args.engine)
+    out = interpret(knl, env, args.bounds_check, variant=args.variant,
+                    engine=args.engine)
     torch.cuda.synchronize(dev)
     t1 = time.perf_counter()
     outs = _kv(args.outputs, "--out", str)
@@ -201,6 +243,11 @@ def main(argv=None):
     p = sub.add_parser("check")
     common(p)
     p.add_argument("--param", action="append")
+    p.add_argument("--smoke", action="store_true",
+                   help="with --param: run both device engines on seeded "
+                        "inputs and compare (exit 1 on disagreement)")
+    p.add_argument("--seed", type=int, default=0)
+    p.add_argument("--device", type=int, default=0)
     p.set_defaults(fn=cmd_check)
     p = sub.add_parser("run")
     common(p)
@@ -217,6 +264,9 @@ def main(argv=None):
                    default="auto")
     p.add_argument("--variant", type=int, default=0)
     p.add_argument("--device", type=int, default=0)
+    p.add_argument("--bounds-check", action="store_true",
+                   help="interpret_bounds_checked: every subscript checked "
+                        "on the device (interp.py:403)")
     p.add_argument("-v", "--verbose", action="store_true")
     p.set_defaults(fn=cmd_run)
     args = ap.parse_args(argv)

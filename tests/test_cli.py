@@ -5,6 +5,7 @@ golden files byte for byte, the front-end modes, the exit codes.  GPU tests:
 interpret() results."""
 
 import filecmp
+import json
 import os
 import subprocess
 import sys
@@ -149,3 +150,43 @@ def test_cli_run_matches_reference_goldens(cuda, name, tmp_path):
         want = g.out(a)
         assert got.shape == want.shape
         assert got.tobytes() == want.tobytes(), a
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("src,params", [
+    (fx.semlap_source(8, block=2), {"nelt": 6}),
+    (fx.matvec_source("f64"), {"n": 256}),
+    (fx.axpy_source("f32"), {"n": 333}),
+    (fx.gemm_source("f64"), {"m": 40, "n": 24, "l": 48}),
+], ids=["semlap8", "matvec", "axpy32", "dgemm"])
+def test_cli_check_smoke_engines_agree(cuda, src, params, tmp_path, capsys):
+    """check --smoke: hand-written kernel vs generated CUDA on the device,
+    same seeded inputs: bitwise, or within the tolerance where the default
+    kernel reassociates (matvec split-j, DMMA GEMM)."""
+    path = _src(tmp_path, src, "k.f")
+    argv = ["check", path, "--smoke"]
+    for k, v in params.items():
+        argv += ["--param", f"{k}={v}"]
+    assert main(argv) == 0
+    rep = json.loads(capsys.readouterr().out)
+    assert rep["smoke"]["agree"]
+    if "semlap" in src or "axpy" in src:
+        assert rep["smoke"]["bitwise"]
+
+
+@pytest.mark.gpu
+def test_cli_run_bounds_check(cuda, tmp_path):
+    """run --bounds-check: the checked device build, same bits."""
+    g = Golden("gen_dgemm_m20_n12_l40")
+    src = _src(tmp_path, g.source(), "dgemm.f")
+    argv = ["run", src, "--bounds-check", "--flat-out"]
+    for k, v in g.params.items():
+        argv += ["--param", f"{k}={v}"]
+    for a in g.args:
+        p = os.path.join(g.dir, f"{a}.in.bin")
+        if os.path.exists(p):
+            argv += ["--in", f"{a}={p}"]
+    argv += ["--out", f"c={tmp_path}/c.bin"]
+    assert main(argv) == 0
+    assert read_array_file(f"{tmp_path}/c.bin").tobytes() == \
+        g.out("c").tobytes()
