@@ -790,6 +790,19 @@ def other_bench(args, local):
         r = run_timed(GenericLauncher(kg, env).launch, None, 2.0 * m * nn * l)
         rows["dgemm_paper_script_2048^3"] = {"TFLOP/s": r["tflops"],
                                              "ms": r["ms_per_step"]}
+        # the SEM fixture itself through the generated CUDA: the
+        # reference's schedule gives one work-item per element with its
+        # wr/ws/wt temporaries (3 n^3 doubles) in private (local) memory --
+        # what a transform outside the recognised set costs
+        ns, ne = 8, 1 << 16
+        _r, ks = fx.translate(fx.semlap_source(ns))
+        u, d, g, w = sem_buffers(ns, ne, dev, ns)
+        env = lfb.env_from_buffers(ks, {"nelt": ne},
+                                   {"u": u, "d": d, "g": g, "w": w})
+        r = run_timed(GenericLauncher(ks, env).launch, 64 * ns ** 3 * ne)
+        rows["semlap_o7_65536_elements"] = {
+            "GDOF/s": ne * ns ** 3 / (r["ms_per_step"] * 1e-3) / 1e9,
+            "frac": r["roofline"]["frac"], "ms": r["ms_per_step"]}
         return {"metric": "generic engine (generated CUDA) GB/s | TFLOP/s",
                 "rows": rows, "engine": "generic (cudagen.py, NVRTC sm_100a)"}
     if wl == "sweep":
