@@ -309,10 +309,23 @@ def make_launcher(kernel, env, variant=0, engine="auto"):
                                "(no CPU fallback)") from exc2
 
 
+_CHECKED_KERNELS = {}  # id(kernel) -> kernel that passed _never_written
+
+
 def _never_written(kernel):
     """interp.py:272-291 raises on a read of a temporary no instruction
     wrote; here the same condition is found before the launch: a
     temporary read by some instruction and written by none."""
+    hit = _CHECKED_KERNELS.get(id(kernel))
+    if hit is kernel:
+        return
+    _never_written_scan(kernel)
+    if len(_CHECKED_KERNELS) > 512:
+        _CHECKED_KERNELS.clear()
+    _CHECKED_KERNELS[id(kernel)] = kernel
+
+
+def _never_written_scan(kernel):
     from ._loopforge import ex, transforms
     k = transforms.expand_all_rules(kernel) if kernel.rules else kernel
     written = set()

@@ -73,21 +73,43 @@ def opencl_guard_constraints(kernel):
     return guards
 
 
-def launch_geometry(kernel, params):
-    """Logical launch geometry of *kernel* at parameter values *params*."""
+_STATIC = {}  # id(kernel) -> (kernel, per-iname bounds, guards, guard text)
+
+
+def _static_geometry(kernel):
+    """The parameter-independent part of the geometry: the reference's
+    bounds (``loop_bounds``, Fourier-Motzkin on the domain, SURVEY.md §8(a)
+    row a5: ~81 % of interpret() time) and the guard constraints, computed
+    once per kernel (kernels are immutable) instead of on every launch."""
+    hit = _STATIC.get(id(kernel))
+    if hit is not None and hit[0] is kernel:
+        return hit[1:]
     k = _expanded(kernel)
-    parallel = codegen.parallel_inames_of(k)
-    groups = [1, 1, 1]
-    local = [1, 1, 1]
-    ng = nl = 0
-    tags = []
-    for iname in parallel:
+    bounds = []
+    for iname in codegen.parallel_inames_of(k):
         tag = k.iname_tags[iname]
         kind, axis = tag.split(".")
         axis = int(axis)
         if axis > 2:
             raise CodegenError(f"tag {tag} on '{iname}': CUDA has 3 axes")
         lowers, uppers = codegen.loop_bounds(k, iname, [])
+        bounds.append((iname, tag, kind, axis, lowers, uppers))
+    guards = opencl_guard_constraints(kernel)
+    text = " && ".join(codegen.render_constraint_c(c) for c in guards)
+    if len(_STATIC) > 512:
+        _STATIC.clear()
+    _STATIC[id(kernel)] = (kernel, tuple(bounds), tuple(guards), text)
+    return tuple(bounds), tuple(guards), text
+
+
+def launch_geometry(kernel, params):
+    """Logical launch geometry of *kernel* at parameter values *params*."""
+    bounds, guards, text = _static_geometry(kernel)
+    groups = [1, 1, 1]
+    local = [1, 1, 1]
+    ng = nl = 0
+    tags = []
+    for iname, tag, kind, axis, lowers, uppers in bounds:
         lo = max(b.eval(params) for b in lowers)
         hi = min(b.eval(params) for b in uppers)
         if lo != 0:
@@ -105,8 +127,6 @@ def launch_geometry(kernel, params):
             groups[axis] = max(hi + 1, 0)
             ng = max(ng, axis + 1)
         tags.append((iname, tag))
-    guards = opencl_guard_constraints(kernel)
-    text = " && ".join(codegen.render_constraint_c(c) for c in guards)
     return Geometry(tuple(groups), tuple(local), ng, nl, bool(guards), text,
                     tuple(tags))
 
