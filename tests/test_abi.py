@@ -74,3 +74,20 @@ def test_built_for_sm100a():
     out = subprocess.run(["cuobjdump", "--list-elf", LIB],
                          capture_output=True, text=True).stdout
     assert "sm_100a" in out
+
+
+def test_missing_library_fails_loudly():
+    """No CPU fallback: without the built .so the executor raises."""
+    import subprocess
+    import sys
+    code = ("from paper_1503_07659_b200 import abi\n"
+            "abi.LIB = '/nonexistent/libloopforge_b200.so'\n"
+            "try:\n"
+            "    abi.load()\n"
+            "except Exception as e:\n"
+            "    print(type(e).__name__, e)\n")
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True,
+                       text=True, timeout=300,
+                       cwd=os.path.dirname(os.path.dirname(
+                           os.path.abspath(__file__))))
+    assert "InterpError" in r.stdout and "no CPU fallback" in r.stdout
