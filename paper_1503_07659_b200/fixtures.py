@@ -313,6 +313,40 @@ end
       '! mvacc = lp.extract_subst(mvacc, "x_acc", "x[jj]", '
       'parameters="jj")\n',
       '! mvacc = lp.precompute(mvacc, "x_acc", "j_inner")\n']),
+    # a 3-point smoother whose u window is precomputed into a workgroup
+    # tile (extent 66 = 64 + 2 halo): a 1-D footprint -> 1-D TMA box
+    "smooth": ("""subroutine smooth(r, u, n)
+  implicit none
+  real*8 r(n), u(n+2)
+  integer n, i
+
+  do i = 1, n
+    r(i) = u(i) + 2*u(i+1) + u(i+2)
+  end do
+end
+""", [_SPLIT.format(k="smooth", i="i", b=64, a=0),
+      '! smooth = lp.assume(smooth, "n mod 64 = 0")\n',
+      '! smooth = lp.extract_subst(smooth, "u_acc", "u[j]", '
+      'parameters="j")\n',
+      '! smooth = lp.precompute(smooth, "u_acc", "i_inner")\n']),
+    # tiled transpose through a workgroup tile (2-D footprint; the tile is
+    # written along a's rows and read down its columns)
+    "ttile": ("""subroutine ttile(b, a, n, m)
+  implicit none
+  real*8 b(m,n), a(n,m)
+  integer n, m, i, j
+
+  do j = 1, m
+    do i = 1, n
+      b(j,i) = a(i,j)
+    end do
+  end do
+end
+""", [_SPLIT.format(k="ttile", i="i", b=16, a=1),
+      _SPLIT.format(k="ttile", i="j", b=16, a=0),
+      '! ttile = lp.extract_subst(ttile, "a_acc", "a[p, q]", '
+      'parameters="p, q")\n',
+      '! ttile = lp.precompute(ttile, "a_acc", "i_inner, j_inner")\n']),
 }
 
 # native-language kernels (kernel.py:323 make_kernel): reductions

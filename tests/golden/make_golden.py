@@ -80,6 +80,16 @@ CASES = {
                               18),
     "gen_rowsum_n40_m17": ("generic_native", {"name": "rowsum"},
                            {"n": 40, "m": 17}, {}, 19),
+    # precompute footprints fetched by TMA on the device: 1-D window with
+    # halo; 2-D tile read down its columns (swizzled), ragged (m = 21) with
+    # a TMA-able leading dimension (n = 40) and one that is not (n = 37:
+    # 296-B rows, cooperative fallback)
+    "gen_smooth_n320": ("generic_source", {"name": "smooth"}, {"n": 320},
+                        {}, 20),
+    "gen_ttile_n40_m21": ("generic_source", {"name": "ttile"},
+                          {"n": 40, "m": 21}, {}, 21),
+    "gen_ttile_n37_m21": ("generic_source", {"name": "ttile"},
+                          {"n": 37, "m": 21}, {}, 22),
 }
 
 # in/out arrays: outputs that are also read (make_env never randomises

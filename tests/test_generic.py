@@ -209,3 +209,21 @@ def test_generic_dgemm_larger(m, n, l, tma, cuda):
     assert got.tobytes() == want.tobytes()
 
 # }}}
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,tma", [("gen_smooth_n320", True),
+                                      ("gen_ttile_n40_m21", True),
+                                      ("gen_ttile_n37_m21", False),
+                                      ("gen_dgemm_m20_n12_l40", True)])
+def test_precompute_footprint_paths(name, tma, cuda):
+    """Which fetch path the goldens exercise: TMA tensor maps when the
+    array meets the tensor-map rules, else the cooperative fetch of the
+    same kernel (both bitwise the reference, test above)."""
+    from paper_1503_07659_b200.generic import GenericLauncher
+    g = Golden(name)
+    _raw, knl = g.kernels()
+    env = _env(g, knl, cuda)
+    launcher = GenericLauncher(knl, env)
+    assert launcher.program.tma
+    assert launcher.tensor_maps(env)[1] is tma
