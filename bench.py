@@ -790,6 +790,31 @@ def other_bench(args, local):
         r = run_timed(GenericLauncher(kg, env).launch, None, 2.0 * m * nn * l)
         rows["dgemm_paper_script_2048^3"] = {"TFLOP/s": r["tflops"],
                                              "ms": r["ms_per_step"]}
+        # precompute footprints by TMA on streaming kernels: the 3-point
+        # smoother's 66-element halo window, and the tiled transpose whose
+        # 16x16 tile is read down its columns (128-B swizzle)
+        _r, km = fx.translate(fx.generic_source("smooth"))
+        envs = []
+        for _ in range(3):
+            uu = torch.rand(n + 2, dtype=torch.float64, device=dev,
+                            generator=gen)
+            rr = torch.empty(n, dtype=torch.float64, device=dev)
+            envs.append(lfb.env_from_buffers(km, {"n": n},
+                                             {"r": rr, "u": uu}))
+        r = run_rotating([GenericLauncher(km, e).launch for e in envs],
+                         16 * n)
+        rows["smooth_tma_f64_2^24"] = {"GB/s": r["roofline"]["achieved"],
+                                       "frac": r["roofline"]["frac"]}
+        nt = 8192
+        _r, kt = fx.translate(fx.generic_source("ttile"))
+        at = torch.rand(nt * nt, dtype=torch.float64, device=dev,
+                        generator=gen)
+        bt = torch.empty(nt * nt, dtype=torch.float64, device=dev)
+        env = lfb.env_from_buffers(kt, {"n": nt, "m": nt},
+                                   {"a": at, "b": bt})
+        r = run_timed(GenericLauncher(kt, env).launch, 16 * nt * nt)
+        rows["transpose_tile_tma_f64_8192^2"] = {
+            "GB/s": r["roofline"]["achieved"], "frac": r["roofline"]["frac"]}
         # the SEM fixture itself through the generated CUDA: the
         # reference's schedule gives one work-item per element with its
         # wr/ws/wt temporaries (3 n^3 doubles) in private (local) memory --

@@ -224,6 +224,15 @@ class _TmaPlan:
     coord: tuple            # array dim -> AffineExpr origin (fetch inames 0)
 
 
+def _buf_stride(p):
+    """Elements between the two buffers of a double-buffered TMA tile: the
+    tile rounded up to TMA's 128-B destination alignment, or to the
+    1024-B swizzle atom for a swizzled tile (the pattern is of the absolute
+    shared address)."""
+    unit = (1024 if p.swizzle else 128) // p.esize
+    return (p.ext[0] * p.rows + unit - 1) // unit * unit
+
+
 @dataclass
 class Program:
     source: str
@@ -280,6 +289,8 @@ class _Emitter:
         self.pipe_runs = {}    # id(first fetch nest) -> (K, loop, plans)
         self.pipe_buf = {}     # temp -> current-buffer variable
         self.pipe_temps = set()
+        self.pipe_nbuf = {}    # temp -> buffers (default 2)
+        self.bar_next = 0      # mbarriers handed out (one per buffer/run)
         for t in k.temporaries.values():
             self.dtypes[t.name] = t.dtype
             if t.shape:
@@ -826,7 +837,7 @@ class _Emitter:
             inner = f"(({inner}) ^ ((({row}) & 7) << {s_}))"
         buf = self.pipe_buf.get(e.array)
         if buf is not None:
-            piece += f" + {p.ext[0] * p.rows} * {buf}"
+            piece += f" + {_buf_stride(p)} * {buf}"
         return f"({inner} + {p.width} * {row}{piece})"
 
     def _tma_nest(self, node):
@@ -872,7 +883,7 @@ class _Emitter:
         return p
 
     def _emit_tma_issue(self, plans, cond="lfb_tid == 0", bar="0", buf=None,
-                        subst=None):
+                        subst=None, pre=()):
         """One elected work-item arms barrier *bar* with the byte count and
         issues one TMA per 128-B piece of every footprint (into buffer
         *buf* of a double-buffered tile; *subst* shifts the loop iname for
@@ -880,6 +891,8 @@ class _Emitter:
         total = sum(p.esize * p.ext[0] * p.rows for p in plans)
         self.line(f"if ({cond}) {{")
         self.ind += 1
+        for ln in pre:
+            self.line(ln)
         self.line(f"lfb_expect_tx(&lfb_bars[{bar}], {total}u);")
         for p in plans:
             if p.temp not in self.tma_index:
@@ -897,7 +910,7 @@ class _Emitter:
                     cs[0] = f"(int)({_aff(coord[0])} + {piece * p.width})"
                 off = str(piece * p.width * p.rows)
                 if buf is not None:
-                    off = f"{off} + {p.ext[0] * p.rows} * ({buf})"
+                    off = f"{off} + {_buf_stride(p)} * ({buf})"
                 self.line(f"lfb_tma{rank}(&{p.temp}[{off}], &lfb_tm{m}, "
                           f"{', '.join(cs)}, &lfb_bars[{bar}]);")
         self.ind -= 1
@@ -909,10 +922,16 @@ class _Emitter:
         loop's iname (the paper's k_outer): the next iteration's tiles are
         prefetched into the other buffer while this one is consumed.  Legal
         because the fetched arrays are never written by the kernel."""
+        return self._pipeline_run(node.children, ctx, [node.iname], node)
+
+    def _pipeline_run(self, kids, ctx, moving, node):
+        """The first writer run of *kids* if it is all TMA footprints whose
+        coordinates move with one of the inames *moving* (pushed visible
+        while the nests are checked when *node* is a loop), and the temps
+        are used nowhere outside *node* (None: the whole kernel)."""
         wg = ctx["wg"]
         if not wg or not self.tma_plan:
             return None
-        kids = node.children
         i = 0
         while i < len(kids):
             w, r = self._touches(kids[i], wg)
@@ -927,7 +946,9 @@ class _Emitter:
             if not w or r:
                 break
             j += 1
-        self.visible.append(node.iname)
+        vis = len(self.visible)
+        if node is not None:
+            self.visible.append(node.iname)
         try:
             plans = []
             for c in kids[i:j]:
@@ -938,16 +959,18 @@ class _Emitter:
                     return None
                 plans.append(p)
         finally:
-            self.visible.pop()
-        if not any(node.iname in c.variables for p in plans
+            del self.visible[vis:]
+        if not any(set(moving) & c.variables for p in plans
                    for c in p.coord):
             return None
         temps = {p.temp for p in plans}
-        inside = {self.imap[st.insn_id].id for st in self._walk_stmts(node)}
-        for insn in self.k.instructions:
-            if insn.id not in inside and (
-                    (self._reads(insn) | self._writes(insn)) & temps):
-                return None
+        if node is not None:
+            inside = {self.imap[st.insn_id].id
+                      for st in self._walk_stmts(node)}
+            for insn in self.k.instructions:
+                if insn.id not in inside and (
+                        (self._reads(insn) | self._writes(insn)) & temps):
+                    return None
         for t in temps:
             if t in self.pipe_temps:
                 return None
@@ -972,9 +995,11 @@ class _Emitter:
         self.ind += 1
         self.line(f"const lfb_ix lfb_plo{k} = {lo}, lfb_pup{k} = {up};")
         self.barrier()
+        base = self.bar_next
+        self.bar_next += 2
         self._emit_tma_issue(
             plans, cond=f"lfb_tma && lfb_tid == 0 && lfb_plo{k} <= lfb_pup{k}",
-            bar="0", buf="0",
+            bar=f"{base}", buf="0",
             subst={node.iname: polyset.AffineExpr.var(f"lfb_plo{k}")})
         self.line(f"for (lfb_ix {node.iname} = lfb_plo{k}; {node.iname} <= "
                   f"lfb_pup{k}; ++{node.iname}) {{")
@@ -984,7 +1009,7 @@ class _Emitter:
         self.visible.append(node.iname)
         for t in temps:
             self.pipe_buf[t] = f"lfb_pb{k}"
-        self.pipe_runs[id(first)] = (k, node, plans)
+        self.pipe_runs[id(first)] = (k, node, plans, None, base)
         self.walk_children(node.children, ctx)
         del self.pipe_runs[id(first)]
         for t in temps:
@@ -1204,27 +1229,41 @@ class _Emitter:
                 if tma and pipe is not None:
                     # double-buffered: prefetch the next iteration's tiles
                     # into the other buffer, then wait for this one's
-                    k, loop, plans = pipe
-                    nxt = polyset.AffineExpr.var(loop.iname) + 1
+                    k, loop, plans, gnext, base = pipe
                     self.line("if (lfb_tma) {")
                     self.ind += 1
-                    self._emit_tma_issue(
-                        plans, cond=f"lfb_tid == 0 && {loop.iname} + 1 <= "
-                                    f"lfb_pup{k}",
-                        bar=f"lfb_pb{k} ^ 1", buf=f"lfb_pb{k} ^ 1",
-                        subst={loop.iname: nxt})
-                    self.line(f"lfb_bar_wait(&lfb_bars[lfb_pb{k}], "
-                              f"(lfb_tph >> lfb_pb{k}) & 1u);")
-                    self.line(f"lfb_tph ^= 1u << lfb_pb{k};")
+                    if loop is not None:
+                        nxt = polyset.AffineExpr.var(loop.iname) + 1
+                        self._emit_tma_issue(
+                            plans, cond=f"lfb_tid == 0 && {loop.iname} + 1 "
+                                        f"<= lfb_pup{k}",
+                            bar=f"{base} + (lfb_pb{k} ^ 1)",
+                            buf=f"lfb_pb{k} ^ 1", subst={loop.iname: nxt})
+                    else:   # NB - 1 work-groups ahead of this CTA's
+                        nb = self.pipe_nbuf[plans[0].temp]
+                        ahead = f"lfb_g + {nb - 1} * (lfb_ix)gridDim.x"
+                        subst, pre = gnext(ahead)
+                        nxt = f"(lfb_pb{k} + {nb - 1}) & {nb - 1}"
+                        self._emit_tma_issue(
+                            plans, cond=f"lfb_tid == 0 && {ahead} < lfb_ng",
+                            bar=f"{base} + ({nxt})", buf=nxt, subst=subst,
+                            pre=pre)
+                    cur = f"{base} + lfb_pb{k}"
+                    self.line(f"lfb_bar_wait(&lfb_bars[{cur}], "
+                              f"(lfb_tph >> ({cur})) & 1u);")
+                    self.line(f"lfb_tph ^= 1u << ({cur});")
                     self.ind -= 1
                 elif tma:
                     # TMA when the launcher could encode every tensor map,
                     # else the same tiles fetched cooperatively
+                    b = self.bar_next
+                    self.bar_next += 1
                     self.line("if (lfb_tma) {")
                     self.ind += 1
-                    self._emit_tma_issue([p for _c, p in tma])
-                    self.line("lfb_bar_wait(&lfb_bars[0], lfb_tph & 1u);")
-                    self.line("lfb_tph ^= 1u;")
+                    self._emit_tma_issue([p for _c, p in tma], bar=str(b))
+                    self.line(f"lfb_bar_wait(&lfb_bars[{b}], "
+                              f"(lfb_tph >> {b}) & 1u);")
+                    self.line(f"lfb_tph ^= 1u << {b};")
                     self.ind -= 1
                 if tma:
                     self.line("} else {")
@@ -1417,9 +1456,61 @@ class _Emitter:
         self.line("const lfb_ix lfb_ng = (lfb_ix)(lfb_G0 * lfb_G1 * lfb_G2);")
         self.line("const lfb_ix lfb_g0 = (lfb_ix)lfb_G0, lfb_g1 = (lfb_ix)lfb_G1, "
                   "lfb_g2 = (lfb_ix)lfb_G2;")
-        self.line("for (lfb_ix lfb_g = (lfb_ix)blockIdx.x; lfb_g < lfb_ng; "
-                  "lfb_g += (lfb_ix)gridDim.x) {")
-        self.ind += 1
+        def gnext(gexpr):
+            """Group inames of work-group index *gexpr*, as lfb_nx_*."""
+            subst, pre = {}, []
+            for axis, iname in sorted(gnames.items()):
+                div = " * ".join(f"lfb_g{a}" for a in range(axis)) or "1"
+                pre.append(f"const lfb_ix lfb_nx_{iname} = (({gexpr}) / "
+                           f"({div})) % lfb_g{axis};")
+                subst[iname] = polyset.AffineExpr.var(f"lfb_nx_{iname}")
+            return subst, pre
+
+        gpipe = None
+        if shared and gnames:
+            # tiles of the next work-group this CTA will walk are prefetched
+            # while the current one computes (streaming kernels with one tile
+            # per group are otherwise TMA-latency bound)
+            root = self.tree.children if isinstance(self.tree,
+                                                    codegen.Block) else []
+            found = self._pipeline_run(root, {"wg": shared, "guard": None},
+                                       list(gnames.values()), None)
+            if found is not None:
+                first, plans = found
+                gpipe = (self.pipes, first, plans)
+                self.pipes += 1
+                self.pipe_temps |= {p.temp for p in plans}
+                # ring depth: 4 tiles in flight per CTA when they are small
+                # (streaming kernels: bytes in flight hide TMA latency)
+                tile = sum(_buf_stride(p) * p.esize for p in plans)
+                nb = 4 if tile <= 8192 else 2
+                for p in plans:
+                    self.pipe_nbuf[p.temp] = nb
+        if gpipe is not None:
+            kp, first, plans = gpipe
+            nb = self.pipe_nbuf[plans[0].temp]
+            gbase = self.bar_next
+            self.bar_next += nb
+            for d in range(nb - 1):   # prologue: this CTA's first groups
+                gexpr = "(lfb_ix)blockIdx.x" + (
+                    f" + {d} * (lfb_ix)gridDim.x" if d else "")
+                subst, pre = gnext(gexpr)
+                self._emit_tma_issue(
+                    plans, cond=f"lfb_tma && lfb_tid == 0 && {gexpr} < "
+                                "lfb_ng",
+                    bar=str(gbase + d), buf=str(d), subst=subst, pre=pre)
+            self.line("int lfb_git = 0;  /* groups walked: ring slot */")
+            self.line("for (lfb_ix lfb_g = (lfb_ix)blockIdx.x; lfb_g < "
+                      "lfb_ng; lfb_g += (lfb_ix)gridDim.x, ++lfb_git) {")
+            self.ind += 1
+            self.line(f"const int lfb_pb{kp} = lfb_git & {nb - 1};")
+            for p in plans:
+                self.pipe_buf[p.temp] = f"lfb_pb{kp}"
+            self.pipe_runs[id(first)] = (kp, None, plans, gnext, gbase)
+        else:
+            self.line("for (lfb_ix lfb_g = (lfb_ix)blockIdx.x; lfb_g < "
+                      "lfb_ng; lfb_g += (lfb_ix)gridDim.x) {")
+            self.ind += 1
         for axis, iname in sorted(gnames.items()):
             div = " * ".join(f"lfb_g{a}" for a in range(axis)) or "1"
             self.line(f"const lfb_ix {iname} = (lfb_g / ({div})) % lfb_g{axis};")
@@ -1454,8 +1545,9 @@ class _Emitter:
                 size = 1
                 for s in self.temp_alloc[name]:
                     size *= s
-                if name in self.pipe_temps:
-                    size *= 2                  # double-buffered tile
+                if name in self.pipe_temps:    # multi-buffered tile
+                    size = _buf_stride(self.tma_plan[name]) * \
+                        (self.pipe_nbuf.get(name, 2) - 1) + size
                 q = "__shared__ " if name in shared else ""
                 if name in shared and name in self.tma_plan:
                     q += "__align__(1024) "   # swizzle atoms, TMA dst
@@ -1496,15 +1588,18 @@ class _Emitter:
                 order.append(f"lfb_tm{m}")
             prelude += TMA_PRELUDE + "".join(
                 _tma_fn(r) for r in sorted(self.tma_ranks))
+            nbars = max(1, self.bar_next)
+            if nbars > 32:
+                raise CodegenError("more than 32 TMA barriers in one kernel")
             decl.append("__shared__ __align__(8) unsigned long long "
-                        "lfb_bars[2];")
+                        f"lfb_bars[{nbars}];")
             decl.append("unsigned lfb_tph = 0;  /* phase bit per barrier */")
             chk = " || ".join(f"(lfb_smem({t}) & 1023u)"
                               for t in sorted(self.tma_index))
             pro.append("if (lfb_tma && lfb_tid == 0) {")
             pro.append(f"  if ({chk}) __trap();  /* TMA tiles misaligned */")
-            pro.append("  lfb_bar_init(&lfb_bars[0]);")
-            pro.append("  lfb_bar_init(&lfb_bars[1]);")
+            for b in range(nbars):
+                pro.append(f"  lfb_bar_init(&lfb_bars[{b}]);")
             pro.append("}")
             pro.append("__syncthreads();")
         nthreads = block[0] * block[1] * block[2]

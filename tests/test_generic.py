@@ -227,3 +227,23 @@ def test_precompute_footprint_paths(name, tma, cuda):
     launcher = GenericLauncher(knl, env)
     assert launcher.program.tma
     assert launcher.tensor_maps(env)[1] is tma
+
+
+@pytest.mark.gpu
+def test_group_prefetch_large(cuda):
+    """Enough work-groups that every CTA walks several: the next group's
+    tiles are TMA-prefetched into the second buffer (128-B / 1024-B
+    aligned); results against numpy restatements, bitwise."""
+    n = 64 * 10000
+    _raw, km = fx.translate(fx.generic_source("smooth"), "smooth.f")
+    u = np.random.default_rng(1).random(n + 2)
+    env = lfb.make_device_env(km, {"n": n}, {"u": u}, device=cuda)
+    got = lfb.get_output(lfb.interpret(km, env), "r")
+    want = (u[:-2] + 2.0 * u[1:-1]) + u[2:]
+    assert got.tobytes() == want.tobytes()
+    nt, mt = 1040, 1000
+    _raw, kt = fx.translate(fx.generic_source("ttile"), "ttile.f")
+    a = np.random.default_rng(2).random((nt, mt))
+    env = lfb.make_device_env(kt, {"n": nt, "m": mt}, {"a": a}, device=cuda)
+    got = lfb.get_output(lfb.interpret(kt, env), "b")
+    assert got.tobytes() == np.ascontiguousarray(a.T).tobytes()
