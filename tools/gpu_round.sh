@@ -1,0 +1,11 @@
+#!/bin/bash
+# end-of-round checkpoint: full suite + sanitizers (generic, sem) + every bench line + ncu
+cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
+bash tools/gpu_full.sh
+CS=/usr/local/cuda/bin/compute-sanitizer
+for tool in memcheck racecheck synccheck; do
+  for part in generic sem; do
+    timeout 900 $CS --tool $tool --error-exitcode 9 python tools/sanitize_cases.py $part > gpurun_out/sanitize_${tool}_${part}.log 2>&1
+    echo "$tool $part rc=$?" >> gpurun_out/sanitize_summary.txt
+  done
+done

@@ -103,6 +103,24 @@ def generic_gemm(m, n, l, want_tma):
     return ok
 
 
+def generic_prefetch():
+    """Work-group-level TMA prefetch rings (smoother, tiled transpose) with
+    several groups per CTA."""
+    n = 64 * 6000
+    _r, km = fx.translate(fx.generic_source("smooth"))
+    u = np.random.default_rng(1).random(n + 2)
+    env = lfb.make_device_env(km, {"n": n}, {"u": u}, device=dev)
+    got = lfb.get_output(lfb.interpret(km, env), "r")
+    ok = got.tobytes() == ((u[:-2] + 2.0 * u[1:-1]) + u[2:]).tobytes()
+    _r, kt = fx.translate(fx.generic_source("ttile"))
+    a = np.random.default_rng(2).random((560, 600))
+    env = lfb.make_device_env(kt, {"n": 560, "m": 600}, {"a": a}, device=dev)
+    got = lfb.get_output(lfb.interpret(kt, env), "b")
+    ok &= got.tobytes() == np.ascontiguousarray(a.T).tobytes()
+    print(f"generic prefetch rings: {'ok' if ok else 'MISMATCH'}", flush=True)
+    return ok
+
+
 if __name__ == "__main__":
     which = sys.argv[1] if len(sys.argv) > 1 else "all"
     oks = []
@@ -119,5 +137,6 @@ if __name__ == "__main__":
     if which in ("all", "stream"):
         oks.append(streams())
     if which in ("all", "generic"):
-        oks += [generic_gemm(64, 40, 96, True), generic_gemm(37, 20, 45, False)]
+        oks += [generic_gemm(64, 40, 96, True), generic_gemm(37, 20, 45, False),
+                generic_prefetch()]
     sys.exit(0 if all(oks) else 1)
