@@ -552,6 +552,108 @@ def cpu_reference(n, sample_elems, threads, min_seconds):
                       + f" on {threads} thread(s)",
             "seconds": dt * reps}
 
+def _host_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def cpu_reference_other(wl, threads, min_seconds=2.0):
+    """cpu_baseline for the other BASELINE configs: the reference's emitted
+    C of the same transformed kernel (oracle/_ref, cc -std=c99 -O1) on the
+    host cores.  fill / axpy: index chunks (pointer offsets) on `threads`
+    threads; matvec (rows cannot be split in the emitted signature) and the
+    transformed GEMM: one thread, on a bounded sample stated in `sample`."""
+    import concurrent.futures as cf
+    import ctypes as C
+
+    import numpy as np
+    sys.path.insert(0, os.path.join(REPO, "oracle"))
+    import oracle
+    if not oracle.have_ref():
+        return None
+    P, I, D, F = C.c_void_p, C.c_int, C.c_double, C.c_float
+    rng = np.random.default_rng(0)
+    if wl in ("fill", "axpy"):
+        n = 1 << 24
+        y, x = rng.random(n), rng.random(n)
+        if wl == "fill":
+            fn = oracle.ref_fn("ref_fill_f64", [P, D, I])
+
+            def run(i0, i1):
+                fn(C.c_void_p(y.ctypes.data + 8 * i0), 1.5, i1 - i0)
+        else:
+            fn = oracle.ref_fn("ref_axpy_f64", [P, P, D, I])
+
+            def run(i0, i1):
+                fn(C.c_void_p(y.ctypes.data + 8 * i0),
+                   C.c_void_p(x.ctypes.data + 8 * i0), 1.25, i1 - i0)
+        per = (n + threads - 1) // threads
+        cuts = list(range(0, n, per)) + [n]
+        with cf.ThreadPoolExecutor(threads) as pool:
+            list(pool.map(lambda c: run(cuts[c], cuts[c + 1]),
+                          range(len(cuts) - 1)))
+            t0, reps = time.perf_counter(), 0
+            while True:
+                list(pool.map(lambda c: run(cuts[c], cuts[c + 1]),
+                              range(len(cuts) - 1)))
+                reps += 1
+                if time.perf_counter() - t0 >= min_seconds:
+                    break
+            dt = (time.perf_counter() - t0) / reps
+        nbytes = (8 if wl == "fill" else 24) * n
+        return {"value": nbytes / dt / 1e9, "unit": "GB/s", "cores": threads,
+                "kind": "reference",
+                "sample": f"the full n = 2^24 workload x {reps} rep(s); the "
+                          "reference's emitted C (codegen.emit, cc -std=c99 "
+                          f"-O1) on {threads} thread(s), index chunks",
+                "seconds": dt * reps}
+    if wl == "matvec":
+        n = 4096
+        y, a, x = np.zeros(n), rng.random(n * n), rng.random(n)
+        fn = oracle.ref_fn("ref_matvec_f64", [P, P, P, I])
+        fn(y.ctypes.data_as(P), a.ctypes.data_as(P), x.ctypes.data_as(P), n)
+        t0, reps = time.perf_counter(), 0
+        while True:
+            fn(y.ctypes.data_as(P), a.ctypes.data_as(P),
+               x.ctypes.data_as(P), n)
+            reps += 1
+            if time.perf_counter() - t0 >= min_seconds:
+                break
+        dt = (time.perf_counter() - t0) / reps
+        return {"value": (8 * n * n + 16 * n) / dt / 1e9, "unit": "GB/s",
+                "cores": 1, "kind": "reference",
+                "sample": f"the full 4096^2 workload x {reps} rep(s); the "
+                          "reference's emitted C on 1 thread (its row loop "
+                          "cannot be split through the emitted signature)",
+                "seconds": dt * reps}
+    if wl in ("sgemm", "dgemm"):
+        m = nn = l = 256
+        dt_ = np.float32 if wl == "sgemm" else np.float64
+        a = rng.random(m * l).astype(dt_)
+        b = rng.random(l * nn).astype(dt_)
+        c = rng.random(m * nn).astype(dt_)
+        fn = oracle.ref_fn("ref_sgemm_f32" if wl == "sgemm" else
+                           "ref_dgemm_f64",
+                           [F if wl == "sgemm" else D, P, P, P, I, I, I])
+        t0, reps = time.perf_counter(), 0
+        while True:
+            fn(1.5, a.ctypes.data_as(P), b.ctypes.data_as(P),
+               c.ctypes.data_as(P), l, m, nn)
+            reps += 1
+            if time.perf_counter() - t0 >= min_seconds:
+                break
+        dt = (time.perf_counter() - t0) / reps
+        return {"value": 2.0 * m * nn * l / dt / 1e12, "unit": "TFLOP/s",
+                "cores": 1, "kind": "reference",
+                "sample": f"a {m}^3 sample of the same transformed kernel "
+                          f"(the paper script's tiles) x {reps} rep(s); the "
+                          "reference's emitted C on 1 thread (8192^3 would "
+                          "take hours)",
+                "seconds": dt * reps}
+    return None
+
 # }}}
 
 
@@ -658,6 +760,8 @@ def other_bench(args, local):
         r.update({"metric": f"{wl} fp64 n=2^24 GB/s", "unit": "GB/s",
                   "value": r["roofline"]["achieved"],
                   "variant": args.variant})
+        if not args.no_cpu:
+            r["cpu_baseline"] = cpu_reference_other(wl, _host_threads())
         return r
     if wl == "matvec":
         n = 4096
@@ -690,6 +794,8 @@ def other_bench(args, local):
                                      "row (8.1 cycles each) + the stream, "
                                      "partly overlapped",
                             "chain_us": n * 8.1 / 1.965e3}
+        if not args.no_cpu:
+            r["cpu_baseline"] = cpu_reference_other(wl, _host_threads())
         return r
     if wl == "sgemm":
         m = n = l = args.gemm_n
@@ -723,6 +829,8 @@ def other_bench(args, local):
                   "tensor_peak_note": "3xTF32: 3 tcgen05 kind::tf32 MMAs "
                   "per product, dense TF32 1.1 PFLOP/s -> 367 TFLOP/s "
                   "fp32-equivalent ceiling"})
+        if not args.no_cpu:
+            r["cpu_baseline"] = cpu_reference_other(wl, _host_threads())
         return r
     if wl == "dgemm":
         m = n = l = args.gemm_n
@@ -753,6 +861,8 @@ def other_bench(args, local):
                              "tolerance": 1e-12},
                   "tensor_peak_note": "FP64 DMMA (mma.sync m8n8k4): "
                   "37 TFLOP/s measured peak (tools/micro/dmma_probe.cu)"})
+        if not args.no_cpu:
+            r["cpu_baseline"] = cpu_reference_other(wl, _host_threads())
         return r
     if wl == "generic":
         # the generic engine (CUDA generated from the schedule, NVRTC) on
