@@ -1213,8 +1213,12 @@ class _Emitter:
                     if not wj or rj:
                         break
                     j += 1
-                self.barrier()
-                tma = []
+                pipe = self.pipe_runs.get(id(children[i]))
+                if pipe is None or pipe[1] is not None:
+                    # (a work-group-level ring needs none: the barrier that
+                    # ends the previous group already freed its buffers)
+                    self.barrier()
+                tma, other = [], False
                 for c2 in children[i:j]:
                     if self._cooperative(c2, wg):
                         self.cooperative += 1
@@ -1223,9 +1227,10 @@ class _Emitter:
                             tma.append((c2, p))
                             continue
                         self._emit_strided(c2, ctx)
+                        other = True
                     else:
                         self.walk(c2, ctx)
-                pipe = self.pipe_runs.get(id(children[i]))
+                        other = True
                 if tma and pipe is not None:
                     # double-buffered: prefetch the next iteration's tiles
                     # into the other buffer, then wait for this one's
@@ -1270,9 +1275,12 @@ class _Emitter:
                     self.ind += 1
                     for c2, _p in tma:
                         self._emit_strided(c2, ctx)
+                    if not other:   # TMA readers synchronise on the mbarrier
+                        self.line("__syncthreads();")
                     self.ind -= 1
                     self.line("}")
-                self.barrier()
+                if other or not tma:
+                    self.barrier()
                 i = j
                 continue
             if w and r:
