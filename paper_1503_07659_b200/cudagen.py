@@ -1464,13 +1464,22 @@ class _Emitter:
         self.line("const lfb_ix lfb_ng = (lfb_ix)(lfb_G0 * lfb_G1 * lfb_G2);")
         self.line("const lfb_ix lfb_g0 = (lfb_ix)lfb_G0, lfb_g1 = (lfb_ix)lfb_G1, "
                   "lfb_g2 = (lfb_ix)lfb_G2;")
+        top = max(gnames) if gnames else 0
+
+        def gsplit(gexpr, axis):
+            """Index along g.axis of linear work-group *gexpr* (< lfb_ng):
+            no division for axis 0 of a 1-D space, no modulo on the last
+            axis (the runtime 32/64-bit divisions are per-group cost)."""
+            div = " * ".join(f"lfb_g{a}" for a in range(axis))
+            q = f"(({gexpr}) / ({div}))" if div else f"({gexpr})"
+            return q if axis == top else f"({q} % lfb_g{axis})"
+
         def gnext(gexpr):
             """Group inames of work-group index *gexpr*, as lfb_nx_*."""
             subst, pre = {}, []
             for axis, iname in sorted(gnames.items()):
-                div = " * ".join(f"lfb_g{a}" for a in range(axis)) or "1"
-                pre.append(f"const lfb_ix lfb_nx_{iname} = (({gexpr}) / "
-                           f"({div})) % lfb_g{axis};")
+                pre.append(f"const lfb_ix lfb_nx_{iname} = "
+                           f"{gsplit(gexpr, axis)};")
                 subst[iname] = polyset.AffineExpr.var(f"lfb_nx_{iname}")
             return subst, pre
 
@@ -1520,8 +1529,7 @@ class _Emitter:
                       "lfb_ng; lfb_g += (lfb_ix)gridDim.x) {")
             self.ind += 1
         for axis, iname in sorted(gnames.items()):
-            div = " * ".join(f"lfb_g{a}" for a in range(axis)) or "1"
-            self.line(f"const lfb_ix {iname} = (lfb_g / ({div})) % lfb_g{axis};")
+            self.line(f"const lfb_ix {iname} = {gsplit('lfb_g', axis)};")
         for name in sorted(k.temporaries):
             t = k.temporaries[name]
             if not t.shape:
