@@ -247,3 +247,39 @@ def test_group_prefetch_large(cuda):
     env = lfb.make_device_env(kt, {"n": nt, "m": mt}, {"a": a}, device=cuda)
     got = lfb.get_output(lfb.interpret(kt, env), "b")
     assert got.tobytes() == np.ascontiguousarray(a.T).tobytes()
+
+
+@pytest.mark.gpu
+def test_generic_launch_in_cuda_graph(cuda):
+    """A generated kernel with TMA tiles captured in a CUDA graph and
+    replayed: the tensor maps travel as kernel parameters by value."""
+    from paper_1503_07659_b200.generic import GenericLauncher
+    m, n, l = 64, 40, 96
+    _raw, knl = fx.translate(fx.gemm_source("f64"), "dgemm.f")
+    rng = np.random.default_rng(9)
+    a, b, c = rng.random((m, l)), rng.random((l, n)), rng.random((m, n))
+    env = lfb.make_device_env(knl, {"m": m, "n": n, "l": l},
+                              {"a": a, "b": b, "c": c, "alpha": 1.5},
+                              device=cuda)
+    launcher = GenericLauncher(knl, env)
+    c0 = env.arrays["c"].data.clone()
+    s = torch.cuda.Stream(cuda)
+    s.wait_stream(torch.cuda.current_stream(cuda))
+    with torch.cuda.stream(s):
+        launcher.launch()           # warm: compile + module load
+    torch.cuda.current_stream(cuda).wait_stream(s)
+    torch.cuda.synchronize()
+    env.arrays["c"].data.copy_(c0)
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        launcher.launch()
+    env.arrays["c"].data.copy_(c0)
+    graph.replay()
+    graph.replay()                  # c accumulates twice
+    torch.cuda.synchronize()
+    want = c.copy()
+    for _ in range(2):
+        for k in range(l):
+            want = want + (1.5 * b[k, :])[None, :] * a[:, k][:, None]
+    got = lfb.get_output(env, "c")
+    assert got.tobytes() == want.tobytes()
