@@ -32,7 +32,9 @@ __host__ __device__ constexpr uint32_t idesc(int M, int N) {
          ((uint32_t)(M >> 4) << 24);
 }
 
-__global__ void __launch_bounds__(128, 1) probe(int iters, int sw128, float *sink) {
+__global__ void __launch_bounds__(128, 1) probe(int iters, int sw128, float *sink,
+                                               long long *cyc) {
+  const long long c0 = clock64();
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char *smem = reinterpret_cast<unsigned char *>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -90,7 +92,10 @@ __global__ void __launch_bounds__(128, 1) probe(int iters, int sw128, float *sin
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];"
                  : "=r"(v) : "r"(tmem));
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-    if (threadIdx.x == 0) sink[blockIdx.x] = __uint_as_float(v);
+    if (threadIdx.x == 0) {
+      sink[blockIdx.x] = __uint_as_float(v);
+      cyc[blockIdx.x] = clock64() - c0;
+    }
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;"
                  ::"r"(tmem));
   }
@@ -101,6 +106,9 @@ int main() {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   float *sink;
   cudaMalloc(&sink, sms * sizeof(float));
+  long long *cyc;
+  cudaMalloc(&cyc, sms * sizeof(long long));
+  long long hc[1024];
   const int smem = 49152 + 1024 + 64;
   cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        smem);
@@ -110,16 +118,18 @@ int main() {
   for (int sw : {1, 0})
   for (int iters : {1000, 20000, 20000}) {
     cudaEventRecord(e0);
-    probe<<<sms, 128, smem>>>(iters, sw, sink);
+    probe<<<sms, 128, smem>>>(iters, sw, sink, cyc);
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     float ms = 0;
     cudaEventElapsedTime(&ms, e0, e1);
     const double flops = 2.0 * 128 * 256 * 8 * 4.0 * iters * sms;
     const cudaError_t err = cudaGetLastError();
+    cudaMemcpy(hc, cyc, sms * sizeof(long long), cudaMemcpyDeviceToHost);
+    const double mhz = (double)hc[0] / (ms * 1e3);
     printf("%s iters %d: %.3f ms  %.1f TFLOP/s tf32  (%.1f fp32-equivalent "
-           "for 3xTF32)  %s\n", sw ? "SW128" : "SW64 ",
-           iters, ms, flops / ms / 1e9, flops / ms / 1e9 / 3,
+           "for 3xTF32)  SM clock %.0f MHz  %s\n", sw ? "SW128" : "SW64 ",
+           iters, ms, flops / ms / 1e9, flops / ms / 1e9 / 3, mhz,
            cudaGetErrorString(err));
   }
   return 0;
