@@ -283,3 +283,21 @@ def test_generic_launch_in_cuda_graph(cuda):
             want = want + (1.5 * b[k, :])[None, :] * a[:, k][:, None]
     got = lfb.get_output(env, "c")
     assert got.tobytes() == want.tobytes()
+
+
+@pytest.mark.gpu
+def test_generic_wide_build_past_2_31(cuda):
+    """An array of 2^31 + 5 elements: the launcher picks the 64-bit index
+    build and the elements past the int range are written."""
+    from paper_1503_07659_b200.generic import GenericLauncher
+    n = (1 << 31) + 5
+    _raw, kf = fx.translate(fx.fill_source("f32"), "fill.f")
+    out = torch.zeros(n, dtype=torch.float32, device=cuda)
+    env = lfb.env_from_buffers(kf, {"n": n}, {"out": out}, {"a": 0.75})
+    launcher = GenericLauncher(kf, env)
+    assert launcher.narrow(env) is False
+    launcher.launch()
+    torch.cuda.synchronize()
+    idx = torch.tensor([0, (1 << 31) - 1, 1 << 31, n - 1], device=cuda)
+    assert bool((out[idx] == 0.75).all())
+    assert int((out != 0.75).sum()) == 0

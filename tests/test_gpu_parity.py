@@ -533,3 +533,41 @@ def test_sgemm_default_dispatch(cuda):
     assert out.arrays["c"].data.cpu().numpy().tobytes() == ref.tobytes()
 
 # }}}
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("variant", [0, 50])
+def test_semlap_offsets_past_2_31(cuda, variant):
+    """Full-size indexing: 2^20 + 37 elements at n = 8, so g holds
+    3.2e9 doubles and its flat index passes 2^31 at element 699,051 (where
+    the reference's emitted C overflows its int).  Every element is
+    written (no NaN left), and sampled elements on both sides of that
+    boundary, the ends and random places match the oracle: bitwise in the
+    default mode, within 1e-12 of the summed-term magnitude in DFMA mode."""
+    n, nelt = 8, (1 << 20) + 37
+    np3 = n ** 3
+    _raw, knl = fx.translate(fx.semlap_source(n, block=1))
+    u, d, g = _sem_inputs(n, nelt, cuda, 77)
+    w = torch.full_like(u, float("nan"))
+    env = lfb.env_from_buffers(knl, {"nelt": nelt},
+                               {"u": u, "d": d, "g": g, "w": w})
+    lfb.interpret(knl, env, inplace=True, variant=variant)
+    torch.cuda.synchronize()
+    assert not bool(torch.isnan(w).any())
+    cross = (1 << 31) // (6 * np3)
+    es = np.unique(np.concatenate([
+        [0, 1, nelt - 2, nelt - 1, cross - 1, cross, cross + 1,
+         (1 << 31) // np3 % nelt],
+        np.random.default_rng(5).integers(0, nelt, 120)]))
+    dh = d.cpu().numpy()
+    for e in es.tolist():
+        ue = u[e * np3:(e + 1) * np3].cpu().numpy()
+        ge = g[6 * e * np3:6 * (e + 1) * np3].cpu().numpy()
+        we = w[e * np3:(e + 1) * np3].cpu().numpy()
+        ref = oracle.semlap(np.zeros(np3), ue, dh, ge, n, 1)
+        if variant == 0:
+            assert we.tobytes() == ref.tobytes(), e
+        else:
+            mag = oracle.semlap(np.zeros(np3), np.abs(ue), np.abs(dh),
+                                np.abs(ge), n, 1)
+            assert (np.abs(we - ref) <= 1e-12 * mag).all(), e
