@@ -58,8 +58,11 @@ def _worker(rank, world, port, n, nelt, q):
     dist.destroy_process_group()
 
 
-def test_gloo_world2_norm_allreduce():
-    n, nelt, world = 4, 18, 2
+@pytest.mark.parametrize("world", [2, 3, 4])
+def test_gloo_world2_norm_allreduce(world):
+    """world 2 as the contract asks, and 3 / 4 ranks (uneven shards, one
+    rank with a partial block) on the same gloo path."""
+    n, nelt = 4, 18
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
