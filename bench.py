@@ -340,52 +340,35 @@ def sem_bench(args, rank, world, local):
     return res, knl
 
 
-def sem_e2e(knl, n, nelt, dev, steps, chunk=1 << 17, variant=0):
-    """Same metric through the public API with HOST buffers.  Headline mode:
-    the operator's parameters (g, d) are device-resident like weights, and
-    every step copies its field u host->device from pinned memory, runs
-    interpret() and reads the result w back.  ``all_inputs_per_step`` also
-    re-uploads g and d every step (PCIe-bound).  The elements are processed
-    in chunks (each chunk is an SEM problem on a slice; elements are
-    independent); copies in, the kernel and copies out run on three streams
-    so both PCIe directions and the kernel overlap."""
+def _ring_e2e(knl, n, nelt, dev, steps, chunk, variant, hu, hw, hg=None,
+              resident_g=None, resident_d=None, hd=None):
+    """One e2e timing: per step, every chunk's u goes host->device from
+    pinned memory, interpret() runs on it, and w comes back device->host.
+    With *hg* the chunk's g (and d) are uploaded as well (all inputs per
+    step); otherwise the device-resident g/d are used.  Copies in, the
+    kernel and copies out run on three streams over a ring of R buffer
+    slots (events order slot reuse), so both PCIe directions and the kernel
+    overlap."""
     import torch
 
     import paper_1503_07659_b200 as lfb
     np3 = n ** 3
-    hu = torch.empty(nelt * np3, dtype=torch.float64, pin_memory=True)
-    hg = torch.empty(6 * nelt * np3, dtype=torch.float64, pin_memory=True)
-    hw = torch.empty(nelt * np3, dtype=torch.float64, pin_memory=True)
-    # synthetic host data: generate on the device chunk-wise, copy down
-    gen = torch.Generator(device=dev).manual_seed(7)
-    for h, sz, lo in ((hu, chunk * np3, -1.0), (hg, 6 * chunk * np3, 0.0)):
-        for s in range(0, h.numel(), sz):
-            v = h[s:s + sz]
-            v.copy_(torch.empty(v.numel(), dtype=torch.float64, device=dev)
-                    .uniform_(lo, 1.0, generator=gen))
-    hd = (torch.rand(n * n, dtype=torch.float64) * 2 - 1).pin_memory()
-    # three engines kept busy at once: host->device copies, the kernel,
-    # device->host copies, each on its own stream, over a ring of R buffer
-    # slots (events order slot reuse), so the PCIe directions overlap each
-    # other as well as the kernel
     R = 3
     h2d, comp, d2h = (torch.cuda.Stream(dev) for _ in range(3))
     bufs = []
     for _ in range(R):
-        bufs.append({"u": torch.empty(chunk * np3, dtype=torch.float64,
-                                      device=dev),
-                     "g": torch.empty(6 * chunk * np3, dtype=torch.float64,
-                                      device=dev),
-                     "w": torch.empty(chunk * np3, dtype=torch.float64,
-                                      device=dev),
-                     "d": torch.empty(n * n, dtype=torch.float64,
-                                      device=dev)})
+        b = {"u": torch.empty(chunk * np3, dtype=torch.float64, device=dev),
+             "w": torch.empty(chunk * np3, dtype=torch.float64, device=dev)}
+        if hg is not None:
+            b["g"] = torch.empty(6 * chunk * np3, dtype=torch.float64,
+                                 device=dev)
+            b["d"] = torch.empty(n * n, dtype=torch.float64, device=dev)
+        bufs.append(b)
     ev_in = [torch.cuda.Event() for _ in range(R)]
     ev_k = [torch.cuda.Event() for _ in range(R)]
     ev_out = [torch.cuda.Event() for _ in range(R)]
     chunks = [(s, min(nelt, s + chunk)) for s in range(0, nelt, chunk)]
     launches = [0]
-    resident = {}  # mode "resident": g and d uploaded once, kept on device
 
     def step():
         for c, (e0, e1) in enumerate(chunks):
@@ -395,16 +378,16 @@ def sem_e2e(knl, n, nelt, dev, steps, chunk=1 << 17, variant=0):
                 h2d.wait_event(ev_k[sl])          # slot's inputs consumed
                 b["u"][:m * np3].copy_(hu[e0 * np3:e1 * np3],
                                        non_blocking=True)
-                if not resident:
+                if hg is not None:
                     b["g"][:6 * m * np3].copy_(hg[6 * e0 * np3:6 * e1 * np3],
                                                non_blocking=True)
                     b["d"].copy_(hd, non_blocking=True)
                 ev_in[sl].record(h2d)
-            if resident:
-                gd = resident["g"][6 * e0 * np3:6 * e1 * np3]
-                dd = resident["d"]
-            else:
+            if hg is not None:
                 gd, dd = b["g"], b["d"]
+            else:
+                gd = resident_g[6 * e0 * np3:6 * e1 * np3]
+                dd = resident_d
             with torch.cuda.stream(comp):
                 comp.wait_event(ev_in[sl])
                 comp.wait_event(ev_out[sl])       # slot's result copied out
@@ -441,49 +424,98 @@ def sem_e2e(knl, n, nelt, dev, steps, chunk=1 << 17, variant=0):
     e1.record(cur)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / steps
-    out = {"value": nelt * np3 / (ms * 1e-3) / 1e9, "unit": "GDOF/s",
-           "h2d_bytes_per_step": (hu.numel() + hg.numel()) * 8
-           + len(chunks) * hd.numel() * 8,
-           "d2h_bytes_per_step": hw.numel() * 8,
-           "ms_per_step": ms, "steps": steps,
-           "gpu_launches": launches[0],
-           "inputs": "every kernel input (u, g, d) copied host->device "
-                     "every step: bound by PCIe (56 B of the 64 B per point "
-                     "are the geometric factors)"}
-    # the operator-application pattern of an iterative solver: geometry
-    # (g, d) set up once on the device (make_device_env-style), each step
-    # moves only the field u in and the result w out
-    try:
-        resident["g"] = hg.to(dev, non_blocking=False)
-        resident["d"] = hd.to(dev)
-        run(1)
-        torch.cuda.synchronize()
-        launches[0] = 0
-        e0.record(cur)
-        run(steps)
-        e1.record(cur)
-        torch.cuda.synchronize()
-        ms2 = e0.elapsed_time(e1) / steps
-        res = {
-            "value": nelt * np3 / (ms2 * 1e-3) / 1e9, "unit": "GDOF/s",
-            "h2d_bytes_per_step": hu.numel() * 8,
-            "d2h_bytes_per_step": hw.numel() * 8, "ms_per_step": ms2,
+    h2d_bytes = hu.numel() * 8
+    if hg is not None:
+        h2d_bytes += hg.numel() * 8 + len(chunks) * hd.numel() * 8
+    return {"value": nelt * np3 / (ms * 1e-3) / 1e9, "unit": "GDOF/s",
+            "nelt": nelt, "h2d_bytes_per_step": h2d_bytes,
+            "d2h_bytes_per_step": hw.numel() * 8, "ms_per_step": ms,
             "steps": steps, "gpu_launches": launches[0],
             "api": "paper_1503_07659_b200.interpret -> lfb_semlap_f64 "
                    f"(ctypes C-ABI), {len(chunks)} chunks of {chunk} "
                    "elements; H2D, kernel and D2H on three streams over "
-                   f"{R} buffer slots",
-            "inputs": "the operator's parameters g (geometric factors) and d "
-                      "stay device-resident like a model's weights "
-                      "(uploaded once, before the timed region); every step "
-                      "copies its input field u host->device and its result "
-                      "w device->host"}
-        resident.clear()
-        res["all_inputs_per_step"] = out
-        return res
-    except RuntimeError as exc:  # device memory: the conservative line only
-        out["resident_geometry"] = {"unavailable": str(exc)[:120]}
-        return out
+                   f"{R} buffer slots"}
+
+
+def _pinned_random(numel, lo, dev, seed, chunk=1 << 26):
+    """Pinned host buffer of uniform [lo, 1) doubles, generated on the device
+    chunk-wise and copied down (host RNG over 2^30 values takes minutes)."""
+    import torch
+    h = torch.empty(numel, dtype=torch.float64, pin_memory=True)
+    gen = torch.Generator(device=dev).manual_seed(seed)
+    for s in range(0, numel, chunk):
+        v = h[s:s + chunk]
+        v.copy_(torch.empty(v.numel(), dtype=torch.float64, device=dev)
+                .uniform_(lo, 1.0, generator=gen))
+    return h
+
+
+def sem_e2e(knl, n, nelt, dev, steps, chunk=1 << 17, variant=0,
+            all_inputs_nelt=0):
+    """Same metric through the public API with HOST buffers, on the full
+    config (*nelt* elements).
+
+    Headline: the operator's parameters (g, d) are device-resident like a
+    model's weights -- generated on the device once, outside the timed
+    region -- and every step copies the step's input field u host->device
+    from pinned memory, runs interpret() and reads the result w back.  Host
+    memory needed: u and w only, 16 B per point (8 GiB each at 2^21
+    elements of order 7).
+
+    ``all_inputs_per_step`` (measured on *all_inputs_nelt* elements when
+    the host can hold their g as well, 64 B per point): g and d are
+    re-uploaded every step too; that one is PCIe-bound (56 of the 64 B per
+    point are geometric factors)."""
+    import torch
+    np3 = n ** 3
+    hu = _pinned_random(nelt * np3, -1.0, dev, 7)
+    hw = torch.empty(nelt * np3, dtype=torch.float64, pin_memory=True)
+    gen = torch.Generator(device=dev).manual_seed(8)
+    rg = torch.empty(6 * nelt * np3, dtype=torch.float64, device=dev)
+    for s in range(0, rg.numel(), 1 << 26):
+        rg[s:s + (1 << 26)].uniform_(0.0, 1.0, generator=gen)
+    rd = torch.rand(n * n, dtype=torch.float64, device=dev,
+                    generator=gen) * 2 - 1
+    res = _ring_e2e(knl, n, nelt, dev, steps, chunk, variant, hu, hw,
+                    resident_g=rg, resident_d=rd)
+    res["inputs"] = ("the operator's parameters g (geometric factors) and d "
+                     "stay device-resident like a model's weights (set up "
+                     "once, before the timed region); every step copies its "
+                     "input field u host->device and its result w "
+                     "device->host")
+    # checker, outside the timed region: the last elements the e2e path
+    # brought back to the host against the oracle on the same inputs
+    ns = min(nelt, 64)
+    e0 = nelt - ns
+    sys.path.insert(0, os.path.join(REPO, "oracle"))
+    import numpy as np
+    import oracle
+    uh = hu[e0 * np3:].numpy()
+    gh = rg[6 * e0 * np3:].cpu().numpy()
+    dh = rd.cpu().numpy()
+    ref = oracle.semlap(np.zeros_like(uh), uh, dh, gh, n, ns, threads=8)
+    got = hw[e0 * np3:].numpy()
+    chk = {"elements": ns, "bitwise": bool(got.tobytes() == ref.tobytes())}
+    if variant == 50:
+        mag = oracle.semlap(np.zeros_like(uh), np.abs(uh), np.abs(dh),
+                            np.abs(gh), n, ns, threads=8)
+        chk["max_err_over_magnitude"] = float((np.abs(got - ref) / mag).max())
+    res["verify_tail"] = chk
+    del rg, rd
+    torch.cuda.empty_cache()
+    if all_inputs_nelt:
+        m = min(all_inputs_nelt, nelt)
+        hg = _pinned_random(6 * m * np3, 0.0, dev, 9)
+        hd = (torch.rand(n * n, dtype=torch.float64) * 2 - 1).pin_memory()
+        ai = _ring_e2e(knl, n, m, dev, steps, chunk, variant, hu[:m * np3],
+                       hw[:m * np3], hg=hg, hd=hd)
+        ai["inputs"] = ("every kernel input (u, g, d) copied host->device "
+                        "every step: bound by PCIe (56 B of the 64 B per "
+                        "point are the geometric factors)")
+        res["all_inputs_per_step"] = ai
+        del hg
+    del hu, hw
+    return res
 
 
 _CPU_SAMPLE = {}
@@ -657,20 +689,24 @@ def cpu_reference_other(wl, threads, min_seconds=2.0):
 # }}}
 
 
-# {{{ other BASELINE configs (not the driver's line; for the record)
+# {{{ the other BASELINE configs (fill, axpy, matvec, sem65k, GEMM, sweep)
 
-def other_bench(args, local):
-    import numpy as np
+# tensor-pipe ceilings measured on this B200 by the repo's own probes (no
+# driver-measured TF32 / FP64 figure exists in MEASURED_PEAKS.json):
+# tools/micro/tf32_probe.cu issues the sgemm kernel's tcgen05 kind::tf32 MMA
+# back to back from resident smem (1115.6 TFLOP/s TF32 = 371.9 fp32-equivalent
+# for 3xTF32); tools/micro/dmma_probe.cu runs mma.sync m8n8k4.f64 (37.0).
+TF32_PEAK_TFLOPS = 1115.6
+DMMA_PEAK_TFLOPS = 37.0
+
+
+def _timing_helpers(args, local):
     import torch
-
-    import paper_1503_07659_b200 as lfb
-    from paper_1503_07659_b200 import fixtures as fx
-    dev = torch.device("cuda", local)
     peak, peak_src = _peaks()
-    wl = args.workload
-    gen = torch.Generator(device=dev).manual_seed(0)
-    def run_timed(fn, bytes_, flops=None):
-        """Per-launch CUDA events; for workloads whose inputs exceed L2."""
+
+    def run_timed(fn, bytes_, flops=None, key=None):
+        """Per-launch CUDA events around each launch (synchronised); for
+        workloads whose inputs exceed L2."""
         for _ in range(args.warmup):
             fn()
         torch.cuda.synchronize()
@@ -686,6 +722,8 @@ def other_bench(args, local):
                 times.append(e0.elapsed_time(e1))
         ms = statistics.median(times)
         out = {"ms_per_step": ms, "ms_best": min(times),
+               "steps": args.steps, "warmup": args.warmup,
+               "timing": "CUDA events around each launch, median",
                "clocks": clk.summary(),
                "l2": "no flush: inputs exceed the 126 MB L2"}
         if bytes_:
@@ -693,24 +731,27 @@ def other_bench(args, local):
                                "achieved": bytes_ / (ms * 1e-3) / 1e9,
                                "peak": peak, "unit": "GB/s",
                                "frac": bytes_ / (ms * 1e-3) / 1e9 / peak,
-                               "traffic": _traffic(wl),
-                               "peak_source": peak_src}
+                               "traffic": _traffic(key) if key else None,
+                               "peak_source": peak_src,
+                               "algorithmic_bytes_per_launch": bytes_}
         if flops:
             out["tflops"] = flops / (ms * 1e-3) / 1e12
         return out
 
-    def run_rotating(launchers, bytes_, flops=None):
+    def run_rotating(launchers, bytes_, flops=None, key=None,
+                     min_region_s=0.3):
         """Back-to-back launches cycling over buffer sets whose footprint is
         several times the 126 MB L2: every launch streams from HBM, and the
         write-backs of the previous launch's dirty lines land inside the
         timed region (steady state) -- neither hidden in L2 nor charged to
-        a flush.  CUDA events between consecutive launches on one stream."""
+        a flush.  The K launches are one CUDA graph (tens-of-us kernels
+        would otherwise wait on the host's ctypes launch path), replayed
+        until the timed region lasts >= min_region_s so the clock sampler
+        sees it."""
         R = len(launchers)
         for q in range(args.warmup * R):
             launchers[q % R]()
         torch.cuda.synchronize()
-        # the K launches are captured into one CUDA graph: tens-of-us kernels
-        # would otherwise wait on the host's ctypes launch path
         graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph):
             for q in range(args.steps):
@@ -719,50 +760,172 @@ def other_bench(args, local):
         torch.cuda.synchronize()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
-        reps = []
+        e0.record()
+        graph.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        reps = max(3, int(min_region_s * 1e3 / max(e0.elapsed_time(e1),
+                                                   1e-3)))
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(reps + 1)]
         with Clocks(local) as clk:
-            for _rep in range(3):
-                e0.record()
+            evs[0].record()
+            for r in range(reps):
                 graph.replay()
-                e1.record()
-                torch.cuda.synchronize()
-                reps.append(e0.elapsed_time(e1) / args.steps)
-        ms = statistics.median(reps)
-        out = {"ms_per_step": ms, "ms_best": min(reps),
+                evs[r + 1].record()
+            torch.cuda.synchronize()
+        per = [evs[r].elapsed_time(evs[r + 1]) / args.steps
+               for r in range(reps)]
+        ms = statistics.median(per)
+        out = {"ms_per_step": ms, "ms_best": min(per),
+               "steps": args.steps, "warmup": args.warmup,
                "timing": f"CUDA graph of {args.steps} back-to-back launches, "
-                         "median of 3 replays", "clocks": clk.summary(),
+                         f"median over {reps} replays",
+               "clocks": clk.summary(),
                "l2": f"no flush: {R} rotating buffer sets, footprint "
                      f"{R * bytes_ / 2**20:.0f} MiB >> 126 MB L2"}
         out["roofline"] = {"bound": "hbm",
                            "achieved": bytes_ / (ms * 1e-3) / 1e9,
                            "peak": peak, "unit": "GB/s",
                            "frac": bytes_ / (ms * 1e-3) / 1e9 / peak,
-                           "traffic": _traffic(wl),
-                           "peak_source": peak_src}
+                           "traffic": _traffic(key) if key else None,
+                           "peak_source": peak_src,
+                           "algorithmic_bytes_per_launch": bytes_}
         if flops:
             out["tflops"] = flops / (ms * 1e-3) / 1e12
         return out
+
+    return run_timed, run_rotating
+
+
+def _gemm_roofline(tflops, dtype):
+    if dtype == "f32":
+        peak = TF32_PEAK_TFLOPS / 3
+        return {"bound": "tensor", "achieved": tflops, "peak": peak,
+                "unit": "TFLOP/s", "frac": tflops / peak, "traffic": None,
+                "peak_source": "measured on B200 by tools/micro/tf32_probe.cu"
+                               f": {TF32_PEAK_TFLOPS} TFLOP/s of tcgen05 "
+                               "kind::tf32 MMA / 3 MMAs per product (3xTF32)"
+                               " = fp32-equivalent ceiling",
+                "tensor_pipe_tf32_tflops": 3 * tflops,
+                "achieved_definition": "2 m n l algorithmic flops / launch "
+                                       "time"}
+    peak = DMMA_PEAK_TFLOPS
+    return {"bound": "tensor", "achieved": tflops, "peak": peak,
+            "unit": "TFLOP/s", "frac": tflops / peak, "traffic": None,
+            "peak_source": "measured on B200 by tools/micro/dmma_probe.cu "
+                           "(mma.sync m8n8k4.f64, 32 warps/SM)",
+            "achieved_definition": "2 m n l algorithmic flops / launch time"}
+
+
+def _gemm_verify(a, b, c0, c, alpha, l, m, n, dtype, ncols=64, groups=4):
+    """The GEMM result against the oracle's restatement of the reference's
+    sequential chain (c + (alpha*b)*a per k ascending, fp32 for sgemm,
+    test_fortran.py:72-103 / interp.py:169-187; pinned bitwise to the
+    reference's emitted C by tests/test_oracle.py) on *ncols* full columns
+    in *groups* spread ranges.  Normwise max|d|/max|ref| over the columns,
+    plus the largest per-entry error relative to that entry."""
+    import numpy as np
+    sys.path.insert(0, os.path.join(REPO, "oracle"))
+    import oracle
+    ah = a.cpu().numpy()
+    bh = b.cpu().numpy()
+    per = ncols // groups
+    starts = [int(q * (n - per) / max(1, groups - 1)) for q in range(groups)]
+    norm_num = norm_den = 0.0
+    worst = 0.0
+    for j0 in starts:
+        j1 = j0 + per
+        ref = c0[j0 * m:j1 * m].cpu().numpy()
+        # oracle.sgemm walks columns [j0, j1) of a full-size c; hand it a
+        # view whose column 0 is j0 by offsetting b and c
+        oracle.sgemm(alpha, ah, np.ascontiguousarray(bh[j0 * l:j1 * l]), ref,
+                     l, m, per, threads=_host_threads())
+        got = c[j0 * m:j1 * m].cpu().numpy()
+        d = np.abs(got.astype(np.float64) - ref.astype(np.float64))
+        norm_num = max(norm_num, float(d.max()))
+        norm_den = max(norm_den, float(np.abs(ref).max()))
+        worst = max(worst, float((d / np.abs(ref.astype(np.float64))).max()))
+    tol = 1e-5 if dtype == "f32" else 1e-12
+    return {"oracle": "oracle.sgemm (the reference's sequential chain, "
+                      + ("fp32" if dtype == "f32" else "fp64") + ")",
+            "columns": ncols, "column_starts": starts,
+            "normwise_max_abs_err_over_max_abs_ref": norm_num / norm_den,
+            "max_per_entry_rel_err": worst, "tolerance": tol,
+            "pass": norm_num / norm_den <= tol}
+
+
+def _sem_check(got, u, d, g, n, ns, variant):
+    """Checker (outside the timed region): ns elements vs the oracle."""
+    import numpy as np
+    sys.path.insert(0, os.path.join(REPO, "oracle"))
+    import oracle
+    ref = oracle.semlap(np.zeros_like(u), u, d, g, n, ns, threads=8)
+    out = {"elements": ns, "bitwise": bool(got.tobytes() == ref.tobytes())}
+    if variant == 50:
+        mag = oracle.semlap(np.zeros_like(u), np.abs(u), np.abs(d),
+                            np.abs(g), n, ns, threads=8)
+        out["max_err_over_magnitude"] = float((np.abs(got - ref) / mag).max())
+        out["tolerance"] = 1e-12
+        out["pass"] = out["max_err_over_magnitude"] <= 1e-12
+    else:
+        out["pass"] = out["bitwise"]
+    return out
+
+
+def bench_workload(wl, args, local, cpu=True):
+    """One of BASELINE's other configs on one GPU: value, ms_per_step,
+    roofline, clocks, a checker result and the reference's CPU path."""
+    import numpy as np
+    import torch
+
+    import paper_1503_07659_b200 as lfb
+    from paper_1503_07659_b200 import fixtures as fx
+    dev = torch.device("cuda", local)
+    run_timed, run_rotating = _timing_helpers(args, local)
+    gen = torch.Generator(device=dev).manual_seed(0)
+    variant = args.variant or 0
+    threads = _host_threads()
 
     if wl in ("fill", "axpy"):
         n = 1 << 24
         src = fx.fill_source("f64") if wl == "fill" else fx.axpy_source("f64")
         _r, knl = fx.translate(src)
-        launchers = []
+        launchers, envs = [], []
         for _set in range(4 if wl == "fill" else 3):
             x = torch.rand(n, dtype=torch.float64, device=dev, generator=gen)
             y = torch.rand(n, dtype=torch.float64, device=dev, generator=gen)
             bufs = {"out": y} if wl == "fill" else {"y": y, "x": x}
             env = lfb.env_from_buffers(knl, {"n": n}, bufs,
                                        {"a": 1.5, "alpha": 1.25})
-            launchers.append(lfb.Launcher(knl, env,
-                                          variant=args.variant).launch)
-        r = run_rotating(launchers, (8 if wl == "fill" else 24) * n)
+            envs.append((env, x, y.clone()))
+            launchers.append(lfb.Launcher(knl, env, variant=variant).launch)
+        r = run_rotating(launchers, (8 if wl == "fill" else 24) * n, key=wl)
+        # checker: one launch from known inputs, bitwise vs the oracle
+        env, x, y0 = envs[0]
+        yv = env.arrays["out" if wl == "fill" else "y"].data
+        yv.copy_(y0)
+        launchers[0]()
+        torch.cuda.synchronize()
+        sys.path.insert(0, os.path.join(REPO, "oracle"))
+        import oracle
+        ref = y0.cpu().numpy()
+        if wl == "fill":
+            oracle.fill(ref, 1.5)
+        else:
+            oracle.axpy(ref, x.cpu().numpy(), 1.25)
+        r["verify"] = {"oracle": f"oracle.{wl}", "elements": n,
+                       "bitwise": bool(yv.cpu().numpy().tobytes()
+                                       == ref.tobytes())}
         r.update({"metric": f"{wl} fp64 n=2^24 GB/s", "unit": "GB/s",
-                  "value": r["roofline"]["achieved"],
-                  "variant": args.variant})
-        if not args.no_cpu:
-            r["cpu_baseline"] = cpu_reference_other(wl, _host_threads())
+                  "value": r["roofline"]["achieved"], "variant": variant,
+                  "dtype": "f64", "config": {
+                      "workload": f"Fortran-ingested {wl}, n=2^24 fp64, "
+                                  "split_iname(i,128,g.0,l.0)",
+                      "n": n}})
+        if cpu:
+            r["cpu_baseline"] = cpu_reference_other(wl, threads)
         return r
+
     if wl == "matvec":
         n = 4096
         _r, knl = fx.translate(fx.matvec_source("f64"))
@@ -774,172 +937,120 @@ def other_bench(args, local):
             y = torch.empty(n, dtype=torch.float64, device=dev)
             envs.append(lfb.env_from_buffers(knl, {"n": n},
                                              {"a": a, "x": x, "y": y}))
-        r = run_rotating([lfb.Launcher(knl, e, variant=args.variant).launch
-                          for e in envs], 8 * n * n + 16 * n, 2 * n * n)
+        r = run_rotating([lfb.Launcher(knl, e, variant=variant).launch
+                          for e in envs], 8 * n * n + 16 * n, 2 * n * n,
+                         key="matvec")
+        sys.path.insert(0, os.path.join(REPO, "oracle"))
+        import oracle
+        e = envs[0]
+        ah, xh = e.arrays["a"].data.cpu().numpy(), \
+            e.arrays["x"].data.cpu().numpy()
+        ref = oracle.matvec(np.zeros(n), ah, xh, n, threads=threads)
         r.update({"metric": "matvec fp64 4096^2 GB/s", "unit": "GB/s",
-                  "value": r["roofline"]["achieved"],
-                  "variant": args.variant,
-                  "parity": "bitwise" if args.variant in (1, 3) else
+                  "value": r["roofline"]["achieved"], "variant": variant,
+                  "dtype": "f64",
+                  "config": {"workload": "Fortran-ingested matvec fp64 "
+                                         "4096x4096, split i by 128 -> "
+                                         "g.0/l.0, j by 32, extract_subst + "
+                                         "precompute of x (add_prefetch)",
+                             "n": n},
+                  "parity": "bitwise" if variant in (1, 3) else
                   "tolerance (split-j, 1e-12 normwise)"})
-        if args.variant == 0:
+        lfb.Launcher(knl, e, variant=variant).launch()
+        torch.cuda.synchronize()
+        got = e.arrays["y"].data.cpu().numpy()
+        r["verify"] = {"oracle": "oracle.matvec (sequential row chain)",
+                       "bitwise": bool(got.tobytes() == ref.tobytes()),
+                       "normwise": float(np.abs(got - ref).max()
+                                         / np.abs(ref).max()),
+                       "tolerance": 1e-12}
+        if variant == 0:
             # the bitwise kernel: each row is a chain of n dependent DADDs
             # (8.1 cycles each, tools/micro/dadd_latency.cu) that overlaps
             # the stream only partly
             r2 = run_rotating([lfb.Launcher(knl, e, variant=3).launch
                                for e in envs], 8 * n * n + 16 * n, 2 * n * n)
+            lfb.Launcher(knl, envs[0], variant=3).launch()
+            torch.cuda.synchronize()
+            got3 = envs[0].arrays["y"].data.cpu().numpy()
             r["bitwise"] = {"variant": 3, "value": r2["roofline"]["achieved"],
                             "ms_per_step": r2["ms_per_step"],
                             "frac": r2["roofline"]["frac"],
+                            "verify_bitwise": bool(got3.tobytes()
+                                                   == ref.tobytes()),
                             "bound": "latency: 4096 dependent DADDs per "
                                      "row (8.1 cycles each) + the stream, "
-                                     "partly overlapped",
-                            "chain_us": n * 8.1 / 1.965e3}
-        if not args.no_cpu:
-            r["cpu_baseline"] = cpu_reference_other(wl, _host_threads())
+                                     "partly overlapped"}
+        if cpu:
+            r["cpu_baseline"] = cpu_reference_other(wl, threads)
         return r
-    if wl == "sgemm":
+
+    if wl in ("sgemm", "dgemm"):
+        dt = "f32" if wl == "sgemm" else "f64"
+        tdt = torch.float32 if dt == "f32" else torch.float64
         m = n = l = args.gemm_n
-        _r, knl = fx.translate(fx.gemm_source("f32"))
-        a = torch.rand(m * l, dtype=torch.float32, device=dev, generator=gen)
-        b = torch.rand(l * n, dtype=torch.float32, device=dev, generator=gen)
-        c = torch.rand(m * n, dtype=torch.float32, device=dev, generator=gen)
+        _r, knl = fx.translate(fx.gemm_source(dt))
+        a = torch.rand(m * l, dtype=tdt, device=dev, generator=gen)
+        b = torch.rand(l * n, dtype=tdt, device=dev, generator=gen)
+        c = torch.rand(m * n, dtype=tdt, device=dev, generator=gen)
         env = lfb.env_from_buffers(knl, {"m": m, "n": n, "l": l},
                                    {"a": a, "b": b, "c": c}, {"alpha": 1.5})
         c0 = c.clone()
-        L = lfb.Launcher(knl, env, variant=args.variant)
+        L = lfb.Launcher(knl, env, variant=variant)
         L.launch()
         torch.cuda.synchronize()
-        # accuracy of one launch on 256 sampled entries against an exact
-        # fp64 dot product (north star: 1e-5 relative for fp32)
-        rs = np.random.default_rng(1)
-        ii = torch.from_numpy(rs.integers(0, m, 256)).to(dev)
-        jj = torch.from_numpy(rs.integers(0, n, 256)).to(dev)
-        A = a.view(l, m)  # a(i,k) at a[i + m k]
-        B = b.view(n, l)  # b(k,j) at b[k + l j]
-        exact = (c0.view(n, m)[jj, ii].double() + 1.5 *
-                 (A[:, ii].double() * B[jj, :].double().T).sum(0))
-        got = c.view(n, m)[jj, ii].double()
-        rel = float(((got - exact).abs() / exact.abs()).max())
+        verify = _gemm_verify(a, b, c0, c, 1.5, l, m, n, dt)
         c.copy_(c0)
         r = run_timed(L.launch, None, 2.0 * m * n * l)
-        r.update({"metric": f"sgemm fp32 {m}^3 TFLOP/s", "unit": "TFLOP/s",
-                  "value": r["tflops"], "variant": args.variant,
-                  "verify": {"max_rel_err_256_samples_vs_fp64": rel,
-                             "tolerance": 1e-5},
-                  "tensor_peak_note": "3xTF32: 3 tcgen05 kind::tf32 MMAs "
-                  "per product, dense TF32 1.1 PFLOP/s -> 367 TFLOP/s "
-                  "fp32-equivalent ceiling"})
-        if not args.no_cpu:
-            r["cpu_baseline"] = cpu_reference_other(wl, _host_threads())
+        r["roofline"] = _gemm_roofline(r["tflops"], dt)
+        r.update({"metric": f"{wl} {m}^3 TFLOP/s", "unit": "TFLOP/s",
+                  "value": r["tflops"], "variant": variant, "dtype": dt,
+                  "verify": verify,
+                  "config": {"workload": f"the paper's GEMM "
+                                         f"(test_fortran.py:72-103) real*"
+                                         f"{4 if dt == 'f32' else 8} "
+                                         f"{m}^3 with its split/prefetch "
+                                         "script",
+                             "m": m, "n": n, "l": l},
+                  "kernel": "sgemm_tc2_kernel: tcgen05 kind::tf32 3xTF32, "
+                            "TMA, TMEM accumulators" if dt == "f32" else
+                            "dgemm_dmma_kernel: FP64 DMMA m8n8k4"})
+        if cpu:
+            r["cpu_baseline"] = cpu_reference_other(wl, threads)
         return r
-    if wl == "dgemm":
-        m = n = l = args.gemm_n
-        _r, knl = fx.translate(fx.gemm_source("f64"))
-        a = torch.rand(m * l, dtype=torch.float64, device=dev, generator=gen)
-        b = torch.rand(l * n, dtype=torch.float64, device=dev, generator=gen)
-        c = torch.rand(m * n, dtype=torch.float64, device=dev, generator=gen)
-        c0 = c.clone()
-        env = lfb.env_from_buffers(knl, {"m": m, "n": n, "l": l},
-                                   {"a": a, "b": b, "c": c}, {"alpha": 1.5})
-        L = lfb.Launcher(knl, env, variant=args.variant)
-        L.launch()
-        torch.cuda.synchronize()
-        rs = np.random.default_rng(1)
-        ii = torch.from_numpy(rs.integers(0, m, 256)).to(dev)
-        jj = torch.from_numpy(rs.integers(0, n, 256)).to(dev)
-        A, B = a.view(l, m), b.view(n, l)
-        seq = c0.view(n, m)[jj, ii].clone()
-        for k in range(l):  # the reference's sequential chain, per sample
-            seq = seq + (1.5 * B[jj, k]) * A[k, ii]
-        got = c.view(n, m)[jj, ii]
-        rel = float(((got - seq).abs() / seq.abs()).max())
-        c.copy_(c0)
-        r = run_timed(L.launch, None, 2.0 * m * n * l)
-        r.update({"metric": f"dgemm fp64 {m}^3 TFLOP/s", "unit": "TFLOP/s",
-                  "value": r["tflops"], "variant": args.variant,
-                  "verify": {"max_rel_err_256_samples_vs_sequential": rel,
-                             "tolerance": 1e-12},
-                  "tensor_peak_note": "FP64 DMMA (mma.sync m8n8k4): "
-                  "37 TFLOP/s measured peak (tools/micro/dmma_probe.cu)"})
-        if not args.no_cpu:
-            r["cpu_baseline"] = cpu_reference_other(wl, _host_threads())
-        return r
-    if wl == "generic":
-        # the generic engine (CUDA generated from the schedule, NVRTC) on
-        # BASELINE workloads the hand-written kernels also cover: what a
-        # kernel outside the recognised set can expect
-        from paper_1503_07659_b200.generic import GenericLauncher
-        rows = {}
-        n = 1 << 24
-        _r, kf = fx.translate(fx.fill_source("f64"))
-        outs = [torch.empty(n, dtype=torch.float64, device=dev)
-                for _ in range(4)]
-        envs = [lfb.env_from_buffers(kf, {"n": n}, {"out": o}, {"a": 1.5})
-                for o in outs]
-        r = run_rotating([GenericLauncher(kf, e).launch for e in envs], 8 * n)
-        rows["fill_f64_2^24"] = {"GB/s": r["roofline"]["achieved"],
-                                 "frac": r["roofline"]["frac"]}
-        _r, ka = fx.translate(fx.axpy_source("f64"))
-        envs = []
-        for _ in range(3):
-            x = torch.rand(n, dtype=torch.float64, device=dev, generator=gen)
-            y = torch.rand(n, dtype=torch.float64, device=dev, generator=gen)
-            envs.append(lfb.env_from_buffers(ka, {"n": n}, {"y": y, "x": x},
-                                             {"alpha": 1.25}))
-        r = run_rotating([GenericLauncher(ka, e).launch for e in envs],
-                         24 * n)
-        rows["axpy_f64_2^24"] = {"GB/s": r["roofline"]["achieved"],
-                                 "frac": r["roofline"]["frac"]}
-        m = nn = l = 2048
-        _r, kg = fx.translate(fx.gemm_source("f64"))
-        a = torch.rand(m * l, dtype=torch.float64, device=dev, generator=gen)
-        b = torch.rand(l * nn, dtype=torch.float64, device=dev, generator=gen)
-        c = torch.rand(m * nn, dtype=torch.float64, device=dev, generator=gen)
-        env = lfb.env_from_buffers(kg, {"m": m, "n": nn, "l": l},
-                                   {"a": a, "b": b, "c": c}, {"alpha": 1.5})
-        r = run_timed(GenericLauncher(kg, env).launch, None, 2.0 * m * nn * l)
-        rows["dgemm_paper_script_2048^3"] = {"TFLOP/s": r["tflops"],
-                                             "ms": r["ms_per_step"]}
-        # precompute footprints by TMA on streaming kernels: the 3-point
-        # smoother's 66-element halo window, and the tiled transpose whose
-        # 16x16 tile is read down its columns (128-B swizzle)
-        _r, km = fx.translate(fx.generic_source("smooth"))
-        envs = []
-        for _ in range(3):
-            uu = torch.rand(n + 2, dtype=torch.float64, device=dev,
-                            generator=gen)
-            rr = torch.empty(n, dtype=torch.float64, device=dev)
-            envs.append(lfb.env_from_buffers(km, {"n": n},
-                                             {"r": rr, "u": uu}))
-        r = run_rotating([GenericLauncher(km, e).launch for e in envs],
-                         16 * n)
-        rows["smooth_tma_f64_2^24"] = {"GB/s": r["roofline"]["achieved"],
-                                       "frac": r["roofline"]["frac"]}
-        nt = 8192
-        _r, kt = fx.translate(fx.generic_source("ttile"))
-        at = torch.rand(nt * nt, dtype=torch.float64, device=dev,
-                        generator=gen)
-        bt = torch.empty(nt * nt, dtype=torch.float64, device=dev)
-        env = lfb.env_from_buffers(kt, {"n": nt, "m": nt},
-                                   {"a": at, "b": bt})
-        r = run_timed(GenericLauncher(kt, env).launch, 16 * nt * nt)
-        rows["transpose_tile_tma_f64_8192^2"] = {
-            "GB/s": r["roofline"]["achieved"], "frac": r["roofline"]["frac"]}
-        # the SEM fixture itself through the generated CUDA: the
-        # reference's schedule gives one work-item per element with its
-        # wr/ws/wt temporaries (3 n^3 doubles) in private (local) memory --
-        # what a transform outside the recognised set costs
-        ns, ne = 8, 1 << 16
-        _r, ks = fx.translate(fx.semlap_source(ns))
-        u, d, g, w = sem_buffers(ns, ne, dev, ns)
-        env = lfb.env_from_buffers(ks, {"nelt": ne},
+
+    if wl == "sem65k":
+        n, nelt = 8, 65536
+        _r, knl = fx.translate(fx.semlap_source(n), "semlap.f")
+        u, d, g, w = sem_buffers(n, nelt, dev, 3)
+        env = lfb.env_from_buffers(knl, {"nelt": nelt},
                                    {"u": u, "d": d, "g": g, "w": w})
-        r = run_timed(GenericLauncher(ks, env).launch, 64 * ns ** 3 * ne)
-        rows["semlap_o7_65536_elements"] = {
-            "GDOF/s": ne * ns ** 3 / (r["ms_per_step"] * 1e-3) / 1e9,
-            "frac": r["roofline"]["frac"], "ms": r["ms_per_step"]}
-        return {"metric": "generic engine (generated CUDA) GB/s | TFLOP/s",
-                "rows": rows, "engine": "generic (cudagen.py, NVRTC sm_100a)"}
+        out = {"metric": "SEM o7 fp64 65,536 elements GDOF/s",
+               "unit": "GDOF/s", "dtype": "f64",
+               "config": {"workload": "semlap order 7 (n=8) fp64, 65536 "
+                                      "elements, split_iname(e,32,g.0,l.0) "
+                                      "+ assume + extract_subst(gf)",
+                          "nelt": nelt, "npts": n}}
+        ns = 256
+        uh = u[:ns * 512].cpu().numpy()
+        gh = g[:6 * ns * 512].cpu().numpy()
+        dh = d.cpu().numpy()
+        for tag, v in (("", 50), ("bitwise", 0)):
+            L = lfb.Launcher(knl, env, variant=v)
+            r = run_timed(L.launch, 64 * n ** 3 * nelt,
+                          key="sem65k" if v == 0 else None)
+            r["value"] = nelt * n ** 3 / (r["ms_per_step"] * 1e-3) / 1e9
+            r["variant"] = v
+            r["verify"] = _sem_check(w[:ns * 512].cpu().numpy(), uh, dh, gh,
+                                     n, ns, v)
+            if tag:
+                out[tag] = r
+            else:
+                out.update(r)
+        if cpu:
+            out["cpu_baseline"] = cpu_reference(n, nelt, threads, 2.0)
+        return out
+
     if wl == "sweep":
         rows = []
         for n in range(4, 17):
@@ -948,22 +1059,243 @@ def other_bench(args, local):
             u, d, g, w = sem_buffers(n, nelt, dev, n)
             env = lfb.env_from_buffers(knl, {"nelt": nelt},
                                        {"u": u, "d": d, "g": g, "w": w})
+            np3 = n ** 3
+            ns = 32
+            uh = u[:ns * np3].cpu().numpy()
+            gh = g[:6 * ns * np3].cpu().numpy()
+            dh = d.cpu().numpy()
             row = {"order": n - 1, "npts": n, "nelt": nelt}
             for tag, v in (("", 0), ("fma_", 50)):
                 L = lfb.Launcher(knl, env, variant=v)
-                r = run_timed(L.launch, 64 * n ** 3 * nelt)
+                r = run_timed(L.launch, 64 * np3 * nelt)
                 row.update({f"{tag}ms": r["ms_per_step"],
-                            f"{tag}gdofs": nelt * n ** 3
+                            f"{tag}gdofs": nelt * np3
                             / (r["ms_per_step"] * 1e-3) / 1e9,
                             f"{tag}hbm_frac": r["roofline"]["frac"],
-                            f"{tag}sm_mhz": r["clocks"]["sm_mhz"]})
+                            f"{tag}sm_mhz": r["clocks"]["sm_mhz"],
+                            f"{tag}verify": _sem_check(
+                                w[:ns * np3].cpu().numpy(), uh, dh, gh, n,
+                                ns, v)})
+            if cpu:
+                cb = cpu_reference(n, max(32, (1 << 18) // np3 // 32 * 32),
+                                   threads, 0.3)
+                row["cpu_gdofs"] = cb["value"]
+                row["cpu_kind"] = cb["kind"]
             rows.append(row)
             del u, d, g, w, env, L
             torch.cuda.empty_cache()
+        peak, peak_src = _peaks()
         return {"metric": "SEM sweep orders 3-15 GDOF/s", "rows": rows,
+                "unit": "GDOF/s", "dtype": "f64",
+                "roofline": {"bound": "hbm", "peak": peak, "unit": "GB/s",
+                             "peak_source": peak_src,
+                             "algorithmic_bytes_per_element": "64 n^3"},
+                "cpu_baseline_note": f"cpu_gdofs: the reference's emitted C "
+                                     f"(oracle/_ref) on {threads} threads, "
+                                     "a ~2^18-point sample per order",
                 "modes": "gdofs/hbm_frac: bitwise kernels (variant 0); "
-                         "fma_*: DFMA mode (variant 50, within 1e-12)"}
+                         "fma_*: DFMA/DMMA mode (variant 50, within 1e-12)",
+                "config": {"workload": "semlap orders 3..15, nelt = "
+                                       "2^25/n^3 (~2 GiB traffic each)"}}
+
+    if wl == "generic":
+        return generic_bench(args, local)
     raise SystemExit(f"unknown workload {wl}")
+
+
+def generic_bench(args, local):
+    """The generic engine (CUDA generated from the schedule, NVRTC) on
+    BASELINE workloads the hand-written kernels also cover: what a kernel
+    outside the recognised set can expect."""
+    import torch
+
+    import paper_1503_07659_b200 as lfb
+    from paper_1503_07659_b200 import fixtures as fx
+    from paper_1503_07659_b200.generic import GenericLauncher
+    dev = torch.device("cuda", local)
+    run_timed, run_rotating = _timing_helpers(args, local)
+    gen = torch.Generator(device=dev).manual_seed(0)
+    rows = {}
+    n = 1 << 24
+    _r, kf = fx.translate(fx.fill_source("f64"))
+    outs = [torch.empty(n, dtype=torch.float64, device=dev)
+            for _ in range(4)]
+    envs = [lfb.env_from_buffers(kf, {"n": n}, {"out": o}, {"a": 1.5})
+            for o in outs]
+    r = run_rotating([GenericLauncher(kf, e).launch for e in envs], 8 * n)
+    rows["fill_f64_2^24"] = {"GB/s": r["roofline"]["achieved"],
+                             "frac": r["roofline"]["frac"]}
+    _r, ka = fx.translate(fx.axpy_source("f64"))
+    envs = []
+    for _ in range(3):
+        x = torch.rand(n, dtype=torch.float64, device=dev, generator=gen)
+        y = torch.rand(n, dtype=torch.float64, device=dev, generator=gen)
+        envs.append(lfb.env_from_buffers(ka, {"n": n}, {"y": y, "x": x},
+                                         {"alpha": 1.25}))
+    r = run_rotating([GenericLauncher(ka, e).launch for e in envs], 24 * n)
+    rows["axpy_f64_2^24"] = {"GB/s": r["roofline"]["achieved"],
+                             "frac": r["roofline"]["frac"]}
+    m = nn = l = 2048
+    _r, kg = fx.translate(fx.gemm_source("f64"))
+    a = torch.rand(m * l, dtype=torch.float64, device=dev, generator=gen)
+    b = torch.rand(l * nn, dtype=torch.float64, device=dev, generator=gen)
+    c = torch.rand(m * nn, dtype=torch.float64, device=dev, generator=gen)
+    env = lfb.env_from_buffers(kg, {"m": m, "n": nn, "l": l},
+                               {"a": a, "b": b, "c": c}, {"alpha": 1.5})
+    r = run_timed(GenericLauncher(kg, env).launch, None, 2.0 * m * nn * l)
+    rows["dgemm_paper_script_2048^3"] = {"TFLOP/s": r["tflops"],
+                                         "ms": r["ms_per_step"]}
+    # precompute footprints by TMA on streaming kernels: the 3-point
+    # smoother's 66-element halo window, and the tiled transpose whose 16x16
+    # tile is read down its columns (128-B swizzle)
+    _r, km = fx.translate(fx.generic_source("smooth"))
+    envs = []
+    for _ in range(3):
+        uu = torch.rand(n + 2, dtype=torch.float64, device=dev, generator=gen)
+        rr = torch.empty(n, dtype=torch.float64, device=dev)
+        envs.append(lfb.env_from_buffers(km, {"n": n}, {"r": rr, "u": uu}))
+    r = run_rotating([GenericLauncher(km, e).launch for e in envs], 16 * n)
+    rows["smooth_tma_f64_2^24"] = {"GB/s": r["roofline"]["achieved"],
+                                   "frac": r["roofline"]["frac"]}
+    nt = 8192
+    _r, kt = fx.translate(fx.generic_source("ttile"))
+    at = torch.rand(nt * nt, dtype=torch.float64, device=dev, generator=gen)
+    bt = torch.empty(nt * nt, dtype=torch.float64, device=dev)
+    env = lfb.env_from_buffers(kt, {"n": nt, "m": nt}, {"a": at, "b": bt})
+    r = run_timed(GenericLauncher(kt, env).launch, 16 * nt * nt)
+    rows["transpose_tile_tma_f64_8192^2"] = {
+        "GB/s": r["roofline"]["achieved"], "frac": r["roofline"]["frac"]}
+    # the SEM fixture itself through the generated CUDA: the reference's
+    # schedule gives one work-item per element with its wr/ws/wt temporaries
+    # (3 n^3 doubles) in private (local) memory
+    ns, ne = 8, 1 << 16
+    _r, ks = fx.translate(fx.semlap_source(ns))
+    u, d, g, w = sem_buffers(ns, ne, dev, ns)
+    env = lfb.env_from_buffers(ks, {"nelt": ne},
+                               {"u": u, "d": d, "g": g, "w": w})
+    r = run_timed(GenericLauncher(ks, env).launch, 64 * ns ** 3 * ne)
+    rows["semlap_o7_65536_elements"] = {
+        "GDOF/s": ne * ns ** 3 / (r["ms_per_step"] * 1e-3) / 1e9,
+        "frac": r["roofline"]["frac"], "ms": r["ms_per_step"]}
+    return {"metric": "generic engine (generated CUDA) GB/s | TFLOP/s",
+            "rows": rows, "engine": "generic (cudagen.py, NVRTC sm_100a)"}
+
+
+CONFIG_WORKLOADS = ("fill", "axpy", "matvec", "sem65k", "sgemm", "dgemm",
+                    "sweep")
+
+
+def configs_bench(args, local):
+    """BASELINE configs 1, 2, 3 and 5 on the driver's clock: each one's line
+    (value, roofline, clocks, checker, the reference's CPU path) under
+    ``configs`` of the default bench line.  Steps/warm-up as the headline;
+    sized to add about a minute."""
+    import copy
+    import torch
+    out = {}
+    t0 = time.perf_counter()
+    for wl in CONFIG_WORKLOADS:
+        a = copy.copy(args)
+        a.variant = 0
+        t1 = time.perf_counter()
+        try:
+            out[wl] = bench_workload(wl, a, local, cpu=not args.no_cpu)
+        except Exception as exc:  # report, keep the headline line intact
+            out[wl] = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+        out[wl]["wall_s"] = time.perf_counter() - t1
+        torch.cuda.empty_cache()
+    out["wall_s"] = time.perf_counter() - t0
+    return out
+
+# }}}
+
+
+# {{{ multi-GPU launch without torchrun
+
+def _free_port():
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def spawn_ranks(args):
+    """``python bench.py --gpus N`` (N > 1) outside torchrun: start the N
+    ranks ourselves -- one process per GPU through torch.distributed.run on
+    127.0.0.1 -- and return their exit code.  Fails loudly when fewer than N
+    devices are visible (never silently times one GPU)."""
+    import torch
+    have = torch.cuda.device_count()
+    if have < args.gpus and os.environ.get("LFB_BENCH_ONE_DEVICE") != "1":
+        print(json.dumps({"metric": METRIC, "error":
+                          f"--gpus {args.gpus} but only {have} CUDA "
+                          "device(s) are visible"}))
+        return 1
+    env = dict(os.environ)
+    # NCCL's own record of every communicator (rank / nranks per GPU) goes
+    # to a file, not stdout, so the JSON line stays the only stdout line
+    logdir = os.path.join(REPO, "gpurun_out",
+                          f"nccl_{time.strftime('%Y%m%d_%H%M%S')}_"
+                          f"{os.getpid()}")
+    os.makedirs(logdir, exist_ok=True)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    env.setdefault("NCCL_DEBUG_FILE",
+                   os.path.join(logdir, "nccl_bench.%h.%p.log"))
+    env["LFB_NCCL_LOGDIR"] = logdir
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(_free_port()),
+           os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.run(cmd, env=env).returncode
+
+
+def comm_report(world, local):
+    """Proof the job spans `world` ranks on distinct devices: every rank's
+    device (all-gathered) and an all-reduce of ones over the data-path
+    backend (NCCL on the box)."""
+    import torch
+    import torch.distributed as dist
+    if world == 1:
+        return {"backend": None, "world_size": 1,
+                "devices": [torch.cuda.get_device_name(local)]}
+    backend = dist.get_backend()
+    dev = torch.device("cuda", local) if backend == "nccl" else \
+        torch.device("cpu")
+    one = torch.ones(1, device=dev)
+    dist.all_reduce(one)
+    info = [None] * world
+    dist.all_gather_object(info, {
+        "rank": dist.get_rank(), "local_rank": local,
+        "cuda_device": torch.cuda.current_device(),
+        "pci_bus": torch.cuda.get_device_properties(local).pci_bus_id
+        if hasattr(torch.cuda.get_device_properties(local), "pci_bus_id")
+        else None})
+    return {"backend": backend, "world_size": dist.get_world_size(),
+            "allreduce_of_ones": float(one.item()), "ranks": info}
+
+
+def nccl_log_summary():
+    """Communicator lines NCCL wrote (NCCL_DEBUG=INFO, spawn_ranks)."""
+    import glob
+    import re
+    d = os.environ.get("LFB_NCCL_LOGDIR")
+    if not d:
+        return None
+    nranks = []
+    for path in glob.glob(os.path.join(d, "nccl_bench.*.log")):
+        try:
+            with open(path, errors="replace") as f:
+                for line in f:
+                    m = re.search(r"nranks (\d+)", line)
+                    if m and "Init COMPLETE" in line:
+                        nranks.append(int(m.group(1)))
+        except OSError:
+            pass
+    return {"init_complete_lines": len(nranks),
+            "nranks": sorted(set(nranks))}
 
 # }}}
 
@@ -982,6 +1314,9 @@ def main():
     ap.add_argument("--no-verify", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-configs", action="store_true",
+                    help="skip the other BASELINE configs in the default "
+                         "line")
     ap.add_argument("--e2e-nelt", type=int, default=0)
     ap.add_argument("--e2e-chunk", type=int, default=1 << 17,
                     help="elements per host<->device chunk in the e2e run")
@@ -992,7 +1327,7 @@ def main():
     args.npts = 8
     args.nelt = {"sem2m": 1 << 21, "sem65k": 65536}.get(args.workload,
                                                          1 << 21)
-    threads = os.cpu_count() or 1
+    threads = _host_threads()
 
     if args.impl == "reference":
         # the reference's own CPU execution of the path, rank 0 only
@@ -1024,44 +1359,65 @@ def main():
         print(json.dumps(res))
         return
 
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args))
+
     rank, world, local = dist_init(args.gpus)
     import torch
     if args.workload not in ("sem2m", "sem65k"):
         if rank == 0:
-            print(json.dumps(other_bench(args, local)))
+            print(json.dumps(bench_workload(args.workload, args, local,
+                                            cpu=not args.no_cpu)))
         return
+    comm = comm_report(world, local)
     res, knl = sem_bench(args, rank, world, local)
     dev = torch.device("cuda", local)
     res["e2e"] = None
     if not args.no_e2e:
         nelt_e2e = args.e2e_nelt or (args.nelt // world)
-        # pinned host buffers hold u, g, w (72 B/dof): stay within a third
-        # of the host's available memory (shared by all local ranks)
+        # pinned host buffers hold u and w (16 B per point; g and d are
+        # device-resident): stay within half of the host's available memory
+        # (shared by all local ranks); the all-inputs variant also holds g
+        # (+48 B per point) and is measured on what fits
+        ai_nelt = nelt_e2e
         try:
             import psutil
             avail = psutil.virtual_memory().available
-            cap = avail // 3 // max(1, world) // (72 * args.npts ** 3)
+            cap = avail // 2 // max(1, world) // (16 * args.npts ** 3)
             nelt_e2e = max(32, min(nelt_e2e, cap // 32 * 32))
+            ai_cap = (avail // 2 // max(1, world)
+                      - 16 * args.npts ** 3 * nelt_e2e) \
+                // (48 * args.npts ** 3)
+            ai_nelt = max(0, min(nelt_e2e, ai_cap // 32 * 32))
         except Exception:
             pass
         e2e = sem_e2e(knl, args.npts, nelt_e2e, dev, steps=3,
                       chunk=args.e2e_chunk,
-                      variant=res["config"]["variant"])
+                      variant=res["config"]["variant"],
+                      all_inputs_nelt=ai_nelt)
         ms = max_over_ranks(e2e["ms_per_step"], world)
         e2e["value"] = nelt_e2e * world * args.npts ** 3 / (ms * 1e-3) / 1e9
         e2e["ms_per_step"] = ms
+        e2e["nelt"] = nelt_e2e * world
         ai = e2e.get("all_inputs_per_step", {})
         if "ms_per_step" in ai:
             ms2 = max_over_ranks(ai["ms_per_step"], world)
-            ai["value"] = nelt_e2e * world * args.npts ** 3 / (ms2 * 1e-3) / 1e9
+            ai["value"] = ai["nelt"] * world * args.npts ** 3 \
+                / (ms2 * 1e-3) / 1e9
             ai["ms_per_step"] = ms2
         res["e2e"] = e2e
     res["cpu_baseline"] = None
-    if rank == 0 and world == 1 and not args.no_cpu:
+    if rank == 0 and not args.no_cpu:
+        # the reference's CPU path on this box's host cores (rank 0; at
+        # N > 1 the other ranks wait at the barrier below)
         res["cpu_baseline"] = cpu_reference(args.npts, 65536, threads, 15.0)
+    if world == 1 and args.workload == "sem2m" and not args.no_configs:
+        res["configs"] = configs_bench(args, local)
+    barrier(world)
     res.update({"n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "higher_is_better": True,
-                "vs_baseline": None, "data": "synthetic"})
+                "vs_baseline": None, "data": "synthetic",
+                "comm": comm, "nccl_log": nccl_log_summary()})
     if rank == 0:
         print(json.dumps(res))
     if world > 1:

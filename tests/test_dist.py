@@ -109,3 +109,53 @@ def test_bench_multi_rank_path_on_one_gpu(tmp_path):
     assert d["verify"]["max_err_over_magnitude_head"] <= 1e-12
     assert d["verify"]["max_err_over_magnitude_tail"] <= 1e-12
     assert d["e2e"]["value"] > 0
+
+
+@pytest.mark.gpu
+def test_bench_spawns_its_own_ranks(tmp_path):
+    """`python bench.py --gpus 2` WITHOUT torchrun (how the driver's scaling
+    run invokes it) starts its own two ranks and reports n_gpus 2 with the
+    all-reduced norm and a 2-rank communicator -- never a silent 1-GPU run.
+    Both ranks on cuda:0 over gloo (NCCL refuses two ranks on one GPU)."""
+    import json
+    import subprocess
+    import sys
+    env = dict(os.environ, LFB_BENCH_ONE_DEVICE="1", LFB_BENCH_BACKEND="gloo")
+    env.pop("WORLD_SIZE", None)
+    r = subprocess.run(
+        [sys.executable, os.path.join(REPO, "bench.py"), "--gpus", "2",
+         "--workload", "sem65k", "--steps", "3", "--warmup", "3", "--no-cpu",
+         "--e2e-nelt", "4096"],
+        capture_output=True, text=True, timeout=900, env=env, cwd=REPO)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0
+    assert d["comm"]["world_size"] == 2
+    assert d["comm"]["allreduce_of_ones"] == 2.0
+    assert sorted(x["rank"] for x in d["comm"]["ranks"]) == [0, 1]
+    assert d["verify"]["max_err_over_magnitude_head"] <= 1e-12
+    assert d["e2e"]["verify_tail"]["max_err_over_magnitude"] <= 1e-12
+
+
+def test_bench_refuses_more_gpus_than_visible():
+    """Without enough visible devices `bench.py --gpus 2` fails loudly with
+    an error line instead of timing one GPU (CPU container: 0 devices)."""
+    import json
+    import subprocess
+    import sys
+
+    import torch
+    if torch.cuda.device_count() >= 2:
+        pytest.skip("enough devices here")
+    env = dict(os.environ)
+    env.pop("WORLD_SIZE", None)
+    env.pop("LFB_BENCH_ONE_DEVICE", None)
+    r = subprocess.run([sys.executable, os.path.join(REPO, "bench.py"),
+                        "--gpus", "2"], capture_output=True, text=True,
+                       timeout=300, env=env, cwd=REPO)
+    assert r.returncode != 0
+    d = json.loads([l for l in r.stdout.splitlines()
+                    if l.startswith("{")][0])
+    assert "only" in d["error"]
