@@ -34,6 +34,7 @@ import torch
 
 from . import abi
 from ._loopforge import CodegenError, InterpError
+from .inbounds import unproven_access
 from .launch import check_assumptions, launch_geometry
 from .recognize import recognize
 
@@ -214,6 +215,16 @@ class Launcher:
         self.env = env
         w = self.match.workload
         self.npts = w.npts
+        for tp, user in self.match.param_map.items():
+            v = env.params[user]
+            if not -2**31 <= v < 2**31:
+                # the emitted-C ABI passes parameters as C int
+                # (codegen.py:523-525); interp.py uses Python ints, so the
+                # reference runs such a kernel -- make_launcher sends it to
+                # the generic engine's 64-bit build instead
+                raise CodegenError(
+                    f"parameter {user}={v} does not fit the C int of the "
+                    f"{w.name} entry point (emitted-C ABI)")
         self._sumsq = sumsq
         self._workspace = workspace
         if w.name == "gemm" and w.dtype == "f32" and workspace is None \
@@ -238,6 +249,8 @@ class Launcher:
         arrays, scalars, params = env.arrays, env.scalars, env.params
         if stream is None:
             stream = torch.cuda.current_stream(env.device).cuda_stream
+        elif not isinstance(stream, int):
+            stream = stream.cuda_stream
         geom = abi.make_launch(
             self.geometry, npts=w.npts, variant=self.variant,
             sumsq=None if self._sumsq is None else self._sumsq.data_ptr(),
@@ -363,20 +376,38 @@ def interpret(kernel, env, bounds_check=False, *, inplace=False, variant=0,
     checked per dimension against the env's shapes and every temporary
     subscript per dimension; the first violation raises the reference's
     InterpError naming the instruction.  The same checked build (temporaries
-    by flat offset, the reference's plain mode) runs when an env's array
-    shapes no longer match the kernel's declarations -- the case in which
-    the reference's always-on argument checks can fire.  Otherwise the
-    recognised hand-written kernel runs unchecked.
+    by flat offset, the reference's plain mode) runs whenever the
+    reference's always-on argument checks could fire: when an env's array
+    shapes no longer match the kernel's declarations, or when
+    :func:`inbounds.unproven_access` cannot prove every subscript inside
+    its declared extent over the iteration domain.  Otherwise the
+    recognised hand-written kernel (or the unchecked generated one) runs.
     """
     check_assumptions(kernel, env.params)
     _never_written(kernel)
     out = DeviceEnv(dict(env.params), dict(env.arrays), dict(env.scalars),
                     env.device)
+    cloned = []
     if not inplace:
         for a in kernel.args:
             if a.kind == "global-array" and a.is_output:
                 out.arrays[a.name] = env.arrays[a.name].copy()
-    if bounds_check or not _shapes_as_declared(kernel, env):
+                cloned.append(out.arrays[a.name].data)
+    if stream is not None:
+        # the clones above run on the current stream; a launch on another
+        # stream must start after them, and the allocator must know the
+        # clones are used there
+        dev = env.device if env.device is not None else _device(None)
+        cur = torch.cuda.current_stream(dev)
+        s = stream if isinstance(stream, torch.cuda.Stream) else \
+            torch.cuda.ExternalStream(int(stream), device=dev)
+        if s.cuda_stream != cur.cuda_stream:
+            s.wait_stream(cur)
+            for t in cloned:
+                t.record_stream(s)
+        stream = s.cuda_stream
+    if bounds_check or not _shapes_as_declared(kernel, env) \
+            or unproven_access(kernel) is not None:
         from .generic import GenericLauncher
         launcher = GenericLauncher(kernel, out,
                                    checked="dims" if bounds_check

@@ -155,8 +155,11 @@ class GenericLauncher:
         narrow = self.narrow(env)
         with torch.cuda.device(dev):
             mod = _module(prog, dev.index, narrow)
+            cur = torch.cuda.current_stream(dev)
             if stream is None:
-                stream = torch.cuda.current_stream(dev).cuda_stream
+                stream = cur.cuda_stream
+            elif not isinstance(stream, int):
+                stream = stream.cuda_stream
         geo = self.geometry
         if any(int(x) <= 0 for x in geo.group_extent):
             # an empty g.N range: the reference's loop over it runs no
@@ -175,6 +178,11 @@ class GenericLauncher:
                 vals.append(C.c_int32(1 if tma_ok else 0))
             elif name == "lfb_err":
                 err = torch.zeros(16, dtype=torch.int64, device=dev)
+                if stream != cur.cuda_stream:
+                    # zeroed on the current stream, written on `stream`
+                    ext = torch.cuda.ExternalStream(stream, device=dev)
+                    ext.wait_stream(cur)
+                    err.record_stream(ext)
                 vals.append(C.c_void_p(err.data_ptr()))
             elif name.startswith("lfb_x_"):   # checked mode: env extents
                 arr, d = name[6:].rsplit("_", 1)
@@ -205,7 +213,10 @@ class GenericLauncher:
     def _raise_first_oob(self, err, env):
         """The reference's InterpError for the recorded access
         (interp.py:293-308 check_bounds messages)."""
-        rec = err.cpu().tolist()     # synchronises: a debugging mode
+        # the kernel may run on another stream than the current one:
+        # wait for the whole device (a debugging mode) before reading
+        torch.cuda.synchronize(err.device)
+        rec = err.cpu().tolist()
         if not rec[0]:
             return
         prog = self.program

@@ -103,7 +103,17 @@ def _encode(e, inames):
             idx.append(_aff_from_ref(a))
         return ("sub", e.array, tuple(idx))
     if isinstance(e, ex.BinOp):
-        return ("bin", e.op, _encode(e.left, inames), _encode(e.right, inames))
+        left, right = _encode(e.left, inames), _encode(e.right, inames)
+        if e.op in _COMMUTATIVE and _skey(right) < _skey(left):
+            # one IEEE multiply or add gives the same bits with its operands
+            # swapped (and infer_expr_dtype, kernel.py:198-233, promotes
+            # symmetrically), so `x(i)*alpha` is the template's `alpha*x(i)`.
+            # Only this node commutes -- association (expr.py:243-255) is
+            # kept.  The order is by a name-free structural key, so the
+            # canonical renaming that follows stays alpha-invariant; equal
+            # keys keep the written order.
+            left, right = right, left
+        return ("bin", e.op, left, right)
     if isinstance(e, ex.UnOp):
         return ("un", e.op, _encode(e.operand, inames))
     if isinstance(e, ex.Compare):
@@ -115,6 +125,32 @@ def _encode(e, inames):
     if isinstance(e, ex.Reduction):
         return ("red", e.op, e.iname, _encode(e.body, inames))
     raise CodegenError(f"cannot encode expression {e!r}")
+
+
+_COMMUTATIVE = ("+", "*")
+
+
+def _skey(t):
+    """Name-free structural key of an encoded expression: node kinds,
+    operators, literals and affine coefficients, every name erased."""
+    kind = t[0]
+    if kind == "aff":
+        return ("aff", tuple(sorted(c for _n, c in t[1][0])), t[1][1])
+    if kind == "var":
+        return ("var",)
+    if kind == "sub":
+        return ("sub", len(t[2]),
+                tuple((tuple(sorted(c for _n, c in a[0])), a[1])
+                      for a in t[2]))
+    if kind in ("bin", "cmp"):
+        return (kind, t[1], _skey(t[2]), _skey(t[3]))
+    if kind == "un":
+        return ("un", t[1], _skey(t[2]))
+    if kind == "call":
+        return ("call", t[1], tuple(_skey(a) for a in t[2]))
+    if kind == "red":
+        return ("red", t[1], _skey(t[3]))
+    return (kind, repr(t[1:]))
 
 
 def _map_affs(t, fn):

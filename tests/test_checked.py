@@ -128,3 +128,81 @@ def test_bounds_checked_same_results(name, cuda):
     for o in g.outputs():
         assert out.arrays[o].data.cpu().numpy().tobytes() == \
             g.out(o).tobytes(), f"{name}:{o}"
+
+
+OOB_F = """subroutine shift(y, x, n)
+  implicit none
+  real*8 y(n), x(n)
+  integer n, i
+
+  do i = 1, n
+    y(i) = x(i+1)
+  end do
+end
+"""
+
+
+def test_in_bounds_proof():
+    """inbounds.unproven_access: every fixture kernel is proved in bounds
+    (so the fast kernels may run unchecked); a subscript that leaves its
+    declaration is reported."""
+    from paper_1503_07659_b200.inbounds import unproven_access
+    for src in (fx.fill_source("f64"), fx.axpy_source("f32"),
+                fx.matvec_source("f64"), fx.gemm_source("f32"),
+                fx.semlap_source(8), fx.semlap_source(5, block=2)):
+        for knl in fx.translate(src):
+            assert unproven_access(knl) is None
+    _raw, knl = fx.translate(OOB_F)
+    msg = unproven_access(knl)
+    assert msg is not None and "upper bound of x" in msg
+    # an index the rational engine cannot bound: x(2*i) over i <= n
+    _raw, knl = fx.translate(OOB_F.replace("x(i+1)", "x(2*i)"))
+    assert unproven_access(knl) is not None
+
+
+@pytest.mark.gpu
+def test_unproven_kernel_raises_the_reference_error(cuda):
+    """`y(i) = x(i+1)` with x(n) declared.  The reference raises
+    at the first out-of-bounds read (interp.py:293-308, checked whatever
+    bounds_check is); the device path cannot prove the subscript in bounds,
+    so it runs the checked build and raises the same InterpError instead of
+    reading past the buffer."""
+    from paper_1503_07659_b200._loopforge import interp
+    _raw, knl = fx.translate(OOB_F)
+    x = np.arange(8, dtype=np.float64)
+    with pytest.raises(InterpError) as ref_exc:
+        interp.interpret(knl, interp.make_env(knl, {"n": 8}, {"x": x}))
+    env = lfb.make_device_env(knl, {"n": 8}, {"x": x}, device=cuda)
+    with pytest.raises(InterpError) as dev_exc:
+        lfb.interpret(knl, env)
+    assert str(dev_exc.value) == str(ref_exc.value)
+
+
+@pytest.mark.gpu
+def test_side_stream_launch_orders_after_the_clones(cuda):
+    """interpret(..., stream=s) clones the outputs on the current
+    stream, then launches on s; s must wait for the clones (and the
+    allocator must know s uses them).  A big clone makes a missing wait
+    visible; the result is bitwise the oracle's."""
+    import oracle
+    n = 1 << 26
+    _r, knl = fx.translate(fx.axpy_source("f64"))
+    gen = torch.Generator(device=cuda).manual_seed(3)
+    x = torch.rand(n, dtype=torch.float64, device=cuda, generator=gen)
+    y = torch.rand(n, dtype=torch.float64, device=cuda, generator=gen)
+    env = lfb.env_from_buffers(knl, {"n": n}, {"x": x, "y": y},
+                               {"alpha": 1.25})
+    s = torch.cuda.Stream(cuda)
+    for stream in (s, s.cuda_stream):
+        out = lfb.interpret(knl, env, stream=stream)
+        torch.cuda.synchronize()
+        ref = oracle.axpy(y.cpu().numpy(), x.cpu().numpy(), 1.25)
+        assert out.arrays["y"].data.cpu().numpy().tobytes() == ref.tobytes()
+    # checked mode on a side stream still reports the first violation
+    k2 = lfk.make_kernel(["{[i]: 0<=i<n}"], "out[i] = a[i+3]")
+    env2 = lfb.make_device_env(k2, {"n": 6},
+                               {"a": np.ones(9, dtype=np.float32)},
+                               device=cuda)
+    env2.arrays["a"].shape = (4,)
+    with pytest.raises(InterpError, match="insn_0"):
+        lfb.interpret(k2, env2, stream=s)

@@ -402,21 +402,60 @@ def test_assumption_violation_is_interp_error(cuda):
         lfb.make_device_env(knl, {"nelt": 33}, device=cuda)
 
 
+def test_commuted_operands_hit_the_hand_written_kernel(cuda):
+    """`y(i) + x(i)*alpha` is bit-identical to the template's
+    `y(i) + alpha*x(i)` (one IEEE multiply commutes exactly; association,
+    expr.py:243-255, is kept), so it runs lfb_axpy_f64 -- bitwise."""
+    for body in ("y(i) + x(i)*alpha", "x(i)*alpha + y(i)",
+                 "alpha*x(i) + y(i)"):
+        src = fx.axpy_source("f64").replace("y(i) + alpha*x(i)", body)
+        _r, knl = fx.translate(src)
+        assert lfb.recognize(knl).workload.name == "axpy"
+        env = lfb.make_device_env(knl, {"n": 1000}, {"alpha": 1.7}, seed=1,
+                                  device=cuda)
+        out = lfb.interpret(knl, env, engine="kernels")
+        y = env.arrays["y"].data.cpu().numpy()
+        x = env.arrays["x"].data.cpu().numpy()
+        alpha = env.scalars["alpha"]
+        assert out.arrays["y"].data.cpu().numpy().tobytes() == \
+            (y + alpha * x).tobytes(), body
+
+
 def test_unrecognised_kernel_is_codegen_error(cuda):
+    """A re-associated body is a different computation: CodegenError from
+    the hand-written engine, generated CUDA under the default engine."""
     src = fx.axpy_source("f64").replace("y(i) + alpha*x(i)",
-                                        "y(i) + x(i)*alpha")
+                                        "alpha*(x(i) + y(i))")
     _r, knl = fx.translate(src)
     env = lfb.make_device_env(knl, {"n": 256}, {"alpha": 1.7}, seed=1,
                               device=cuda)
     with pytest.raises(CodegenError, match="no CPU fallback"):
         lfb.interpret(knl, env, engine="kernels")
-    # the default engine runs it as generated CUDA instead (test_generic.py)
     out = lfb.interpret(knl, env)
     y = env.arrays["y"].data.cpu().numpy()
     x = env.arrays["x"].data.cpu().numpy()
     alpha = env.scalars["alpha"]
     assert out.arrays["y"].data.cpu().numpy().tobytes() == \
-        (y + x * alpha).tobytes()
+        (alpha * (x + y)).tobytes()
+
+
+def test_parameters_past_2_31_run_on_the_64_bit_build(cuda):
+    """fill with n = 2^31 + 5: the emitted-C ABI's int cannot hold n (the
+    reference interpreter's Python ints can), so interpret() routes the
+    recognised kernel to the generic engine's 64-bit build instead of
+    raising -- every element written, the tail past 2^31 included."""
+    n = (1 << 31) + 5
+    _r, knl = fx.translate(fx.fill_source("f32"))
+    out = torch.zeros(n, dtype=torch.float32, device=cuda)
+    env = lfb.env_from_buffers(knl, {"n": n}, {"out": out}, {"a": 0.75})
+    with pytest.raises(CodegenError, match="C int"):
+        lfb.Launcher(knl, env)
+    lfb.interpret(knl, env, inplace=True)
+    torch.cuda.synchronize()
+    assert int((out == 0.75).sum()) == n
+    assert float(out[-1]) == 0.75 and float(out[(1 << 31) - 1]) == 0.75
+    del out, env
+    torch.cuda.empty_cache()
 
 
 def test_wrong_shape_input_is_interp_error(cuda):
@@ -531,6 +570,56 @@ def test_sgemm_default_dispatch(cuda):
     out = lfb.interpret(knl, env)
     ref = oracle.sgemm(np.float32(0.5), a, b, c.copy(), l, m, n)
     assert out.arrays["c"].data.cpu().numpy().tobytes() == ref.tobytes()
+
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_gemm_8192_cubed_vs_oracle(cuda, dtype):
+    """BASELINE config 5 at its own size: the paper's GEMM script, 8192^3,
+    default dispatch through interpret() (sgemm: tcgen05 3xTF32; dgemm:
+    DMMA), checked on 64 FULL columns (4 spread groups of 16) against the
+    oracle's restatement of the reference's sequential chain
+    c + (alpha*b)*a over ascending k (test_fortran.py:72-103, interp.py:
+    169-187; the oracle is pinned to the reference's emitted C by
+    test_oracle.py).  Tolerance (north star): normwise max|d|/max|ref| <=
+    1e-5 for fp32, 1e-12 for fp64; the fp64 case also per entry against
+    the magnitude sum (|c| + sum_k |alpha b a|)."""
+    m = n = l = 8192
+    np_dt = np.float32 if dtype == "f32" else np.float64
+    _r, knl = fx.translate(fx.gemm_source(dtype))
+    gen = torch.Generator(device=cuda).manual_seed(81)
+    tdt = torch.float32 if dtype == "f32" else torch.float64
+    a = torch.rand(m * l, dtype=tdt, device=cuda, generator=gen)
+    b = torch.rand(l * n, dtype=tdt, device=cuda, generator=gen)
+    c = torch.rand(m * n, dtype=tdt, device=cuda, generator=gen)
+    alpha = np_dt(1.5)
+    env = lfb.env_from_buffers(knl, {"m": m, "n": n, "l": l},
+                               {"a": a, "b": b, "c": c}, {"alpha": alpha})
+    out = lfb.interpret(knl, env)
+    torch.cuda.synchronize()
+    got_all = out.arrays["c"].data
+    ah = a.cpu().numpy()
+    bh = b.cpu().numpy()
+    per = 16
+    worst = 0.0
+    for j0 in (0, 2731, 5461, n - per):
+        cols = slice(j0 * m, (j0 + per) * m)
+        ref = c[cols].cpu().numpy()
+        oracle.sgemm(alpha, ah, np.ascontiguousarray(bh[j0 * l:(j0 + per) * l]),
+                     ref, l, m, per, threads=16)
+        got = got_all[cols].cpu().numpy()
+        d = np.abs(got.astype(np.float64) - ref.astype(np.float64))
+        normwise = d.max() / np.abs(ref).max()
+        worst = max(worst, normwise)
+        if dtype == "f32":
+            assert normwise <= 1e-5, (j0, normwise)
+        else:
+            assert normwise <= 1e-12, (j0, normwise)
+            mag = oracle.sgemm(alpha, np.abs(ah),
+                               np.abs(bh[j0 * l:(j0 + per) * l]).copy(),
+                               np.abs(c[cols].cpu().numpy()), l, m, per,
+                               threads=16)
+            assert (d <= 1e-12 * mag).all(), j0
+    print(f"{dtype} 8192^3: worst normwise error vs the oracle {worst:.2e}")
+
 
 # }}}
 
