@@ -64,8 +64,21 @@ def test_matvec_parallel_reduction_is_rejected():
         recognize(transforms.split_iname(raw, "j", 4, inner_tag="l.0"))
 
 
+def test_commuted_single_node_is_accepted():
+    """a*b == b*a and a+b == b+a bitwise in IEEE arithmetic (one node):
+    these hit the hand-written kernels."""
+    for body in ("y(i) + x(i)*alpha", "x(i)*alpha + y(i)"):
+        src = fx.axpy_source("f64").replace("y(i) + alpha*x(i)", body)
+        raw, _k = fx.translate(src)
+        assert recognize(raw).workload.name == "axpy"
+    src = fx.semlap_source(8).replace("d(i,l)*u(l,j,k,e)", "u(l,j,k,e)*d(i,l)")
+    raw, _k = fx.translate(src)
+    assert recognize(raw).workload.npts == 8
+
+
 def test_reassociated_expression_is_rejected():
-    src = fx.axpy_source("f64").replace("alpha*x(i)", "x(i)*alpha")
+    src = fx.axpy_source("f64").replace("y(i) + alpha*x(i)",
+                                        "(y(i) + alpha)*x(i)")
     raw, _k = fx.translate(src)
     with pytest.raises(CodegenError, match="no CPU fallback"):
         recognize(raw)
