@@ -13,8 +13,12 @@
 // A slot may still be read by a kernel running on another stream, so each
 // slot carries an event: the copy waits for the last kernel that used the
 // slot, and the launch records the event again (dconst_acquire/release).
-// Inside a CUDA graph capture only the copy is recorded (graph order keeps
-// copy and kernel together).
+// Inside a CUDA graph capture the wait and the record become external event
+// wait / record nodes of the graph (cudaEventWaitExternal /
+// cudaEventRecordExternal), so a replayed graph orders its slot copy after
+// the last eager launch (or other graph) that read the slot, and an eager
+// launch after a replay waits for the graph's kernel -- replays and eager
+// launches of the same order with different d may overlap on any streams.
 #pragma once
 
 #include <mutex>
@@ -31,12 +35,12 @@ struct DConstRing {
 };
 
 inline DConstRing &dconst_ring(int tag, int dev) {
-  static DConstRing rings[8][16];
-  return rings[tag & 7][dev & 15];
+  static DConstRing rings[32][16];
+  return rings[tag & 31][dev & 15];
 }
 
 // Copies d (n*n doubles, device memory) to `symbol` at byte offset
-// slot * slot_bytes on stream s, ordered after the last launch that read
+// row_of(slot) * slot_bytes (slot * slot_bytes by default) on stream s, ordered after the last launch that read
 // that slot of ring `tag`.  *slot >= 0 names the slot; *slot = -k picks the
 // next of k rotating slots and returns it.  Returns with the ring locked in
 // *lk; the caller launches on s and then calls dconst_release.
@@ -44,7 +48,7 @@ template <typename T>
 inline int dconst_acquire(const T &symbol, size_t slot_bytes, int tag,
                           int *slot_io, const double *d, int n,
                           cudaStream_t s, std::unique_lock<std::mutex> *lk,
-                          bool *capturing) {
+                          bool *capturing, int (*row_of)(int) = nullptr) {
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess)
     return fail(LFB_ERR_LAUNCH, "semlap: cudaGetDevice failed");
@@ -56,17 +60,20 @@ inline int dconst_acquire(const T &symbol, size_t slot_bytes, int tag,
     r.next = (r.next + 1) % k;
   }
   const int slot = *slot_io;
-  const size_t off = (size_t)slot * slot_bytes;
+  // the slot's row of the constant array (slot itself unless mapped)
+  const size_t off = (size_t)(row_of ? row_of(slot) : slot) * slot_bytes;
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
   cudaStreamIsCapturing(s, &cap);
   *capturing = cap != cudaStreamCaptureStatusNone;
-  if (!*capturing) {
-    if (!r.ev[slot] && cudaEventCreateWithFlags(&r.ev[slot],
-                                                cudaEventDisableTiming) !=
-                           cudaSuccess)
-      return fail(LFB_ERR_LAUNCH, "semlap: event create failed");
-    if (r.used[slot]) cudaStreamWaitEvent(s, r.ev[slot], 0);
-  }
+  if (!r.ev[slot] && cudaEventCreateWithFlags(&r.ev[slot],
+                                              cudaEventDisableTiming) !=
+                         cudaSuccess)
+    return fail(LFB_ERR_LAUNCH, "semlap: event create failed");
+  if (r.used[slot] &&
+      cudaStreamWaitEvent(s, r.ev[slot],
+                          *capturing ? cudaEventWaitExternal : 0) !=
+          cudaSuccess)
+    return fail(LFB_ERR_LAUNCH, "semlap: wait on the d-slot event failed");
   if (cudaMemcpyToSymbolAsync(symbol, d, (size_t)n * n * 8, off,
                               cudaMemcpyDeviceToDevice, s) != cudaSuccess)
     return fail(LFB_ERR_LAUNCH,
@@ -76,11 +83,13 @@ inline int dconst_acquire(const T &symbol, size_t slot_bytes, int tag,
 
 inline void dconst_release(int tag, int slot, cudaStream_t s,
                            bool capturing) {
-  if (capturing) return;
   int dev = 0;
   cudaGetDevice(&dev);
   DConstRing &r = dconst_ring(tag, dev);  // caller still holds r.mu
-  cudaEventRecord(r.ev[slot], s);
+  if (capturing)
+    cudaEventRecordWithFlags(r.ev[slot], s, cudaEventRecordExternal);
+  else
+    cudaEventRecord(r.ev[slot], s);
   r.used[slot] = true;
 }
 

@@ -45,7 +45,11 @@
 
 namespace lfb {
 
-__constant__ double c_dtc[17][256];  // d(a,b) at [N][a + N b]
+// d(a,b) at c_dtc[ROW][a + N b]: ROW = N for the variant-51 kernel and slot
+// 0 of the interleaved-phase kernel, N + 10 for its slot 1 -- two rotating
+// slots per order (dconst.cuh), so same-order launches on two streams do
+// not serialise on one slot
+__constant__ double c_dtc[27][256];
 
 template <int N>
 struct TcCfg {
@@ -82,9 +86,9 @@ __device__ __forceinline__ void dmma(double &d0, double &d1, double a,
       : "d"(a), "d"(b));
 }
 
-template <int N>
+template <int N, int ROW = N>
 __device__ __forceinline__ double dtc(int a, int b) {  // d(a,b), 0 outside
-  return (a < N && b < N) ? c_dtc[N][a + N * b] : 0.0;
+  return (a < N && b < N) ? c_dtc[ROW][a + N * b] : 0.0;
 }
 
 template <int N, int G, int SGS, int KS, bool SUMSQ>
@@ -373,7 +377,8 @@ __device__ __forceinline__ int uidx(int c, int R) {
     return c + N * R;
 }
 
-template <int N, int G, int SGS, int KS, bool SUMSQ, bool SWZ = false>
+template <int N, int G, int SGS, int KS, bool SUMSQ, bool SWZ = false,
+          int ROW = N>
 __global__ void __launch_bounds__(G *TcCfg<N>::T, 1)
     semlap_tc2_kernel(double *__restrict__ w, const double *__restrict__ u,
                       const double *__restrict__ g, int64_t nelt,
@@ -477,10 +482,10 @@ __global__ void __launch_bounds__(G *TcCfg<N>::T, 1)
   double fa_r[KT], fb_s[KT], fa_t[KT], fb_t[KT];
 #pragma unroll
   for (int ks = 0; ks < KT; ++ks) {
-    fa_r[ks] = dtc<N>(8 * it + r, 4 * ks + q);
-    fb_s[ks] = dtc<N>(8 * jt + r, 4 * ks + q);
-    fa_t[ks] = dtc<N>(4 * ks + q, 8 * it + r);
-    fb_t[ks] = dtc<N>(4 * ks + q, 8 * jt + r);
+    fa_r[ks] = dtc<N, ROW>(8 * it + r, 4 * ks + q);
+    fb_s[ks] = dtc<N, ROW>(8 * jt + r, 4 * ks + q);
+    fa_t[ks] = dtc<N, ROW>(4 * ks + q, 8 * it + r);
+    fb_t[ks] = dtc<N, ROW>(4 * ks + q, 8 * jt + r);
   }
 
   double acc_sq = 0.0;
@@ -507,7 +512,7 @@ __global__ void __launch_bounds__(G *TcCfg<N>::T, 1)
       for (int l = 0; l < N; ++l) {
 #pragma unroll
         for (int k = 0; k < N; ++k) {
-          const double dk = c_dtc[N][k + N * l];
+          const double dk = c_dtc[ROW][k + N * l];
           t0[k] = __fma_rn(dk, uc0[l], t0[k]);
           t1[k] = __fma_rn(dk, uc1[l], t1[k]);
         }
@@ -585,7 +590,7 @@ __global__ void __launch_bounds__(G *TcCfg<N>::T, 1)
     for (int l = 0; l < N; ++l) {
 #pragma unroll
       for (int k = 0; k < N; ++k) {
-        const double dk = c_dtc[N][l + N * k];
+        const double dk = c_dtc[ROW][l + N * k];
         p0[k] = __fma_rn(dk, wt0[l], p0[k]);
         p1[k] = __fma_rn(dk, wt1[l], p1[k]);
       }
@@ -633,6 +638,25 @@ static bool make_u_map(CUtensorMap *map, const double *u, int64_t nelt) {
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+template <int N>
+static int slot_row(int slot) { return slot == 0 ? N : N + 10; }
+
+template <int N, int G, int SGS, int KS, int ROW>
+static void tc2_launch_row(bool sumsq, bool swz, int grid, size_t bytes,
+                           double *w, const double *u, const double *g,
+                           int64_t nelt, const lfb_launch *geom,
+                           const CUtensorMap &umap, cudaStream_t s) {
+  auto k = sumsq ? semlap_tc2_kernel<N, G, SGS, KS, true, false, ROW>
+                 : semlap_tc2_kernel<N, G, SGS, KS, false, false, ROW>;
+  auto ks = sumsq ? semlap_tc2_kernel<N, G, SGS, KS, true, N == 16, ROW>
+                  : semlap_tc2_kernel<N, G, SGS, KS, false, N == 16, ROW>;
+  cudaFuncSetAttribute(swz ? ks : k,
+                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)bytes);
+  (swz ? ks : k)<<<grid, G * TcCfg<N>::T, bytes, s>>>(
+      w, u, g, nelt, sumsq ? geom->workspace : nullptr, umap);
+}
+
 template <int N, int G, int SGS, int KS>
 static int launch_tc2(double *w, const double *u, const double *d,
                       const double *g, int64_t nelt, const lfb_launch *geom,
@@ -659,24 +683,23 @@ static int launch_tc2(double *w, const double *u, const double *d,
   memset(&umap, 0, sizeof(umap));
   const bool swz = N == 16 && !(geom && geom->variant == 54) &&
                    make_u_map(&umap, u, nelt);
-  auto k = sumsq ? semlap_tc2_kernel<N, G, SGS, KS, true>
-                 : semlap_tc2_kernel<N, G, SGS, KS, false>;
-  auto ks = sumsq ? semlap_tc2_kernel<N, G, SGS, KS, true, N == 16>
-                  : semlap_tc2_kernel<N, G, SGS, KS, false, N == 16>;
   const size_t bytes = swz ? LS::total : L::total;
-  cudaFuncSetAttribute(swz ? ks : k,
-                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)bytes);
   {
+    // two rotating constant slots per order (rows N and N + 10): one ring
+    // per order, tag 8 + N
     std::unique_lock<std::mutex> lk;
     bool capturing = false;
-    int slot = N;
-    if (int rc = dconst_acquire(c_dtc, 256 * 8, 3, &slot, d, N, s, &lk,
-                                &capturing))
+    int slot = -2;
+    if (int rc = dconst_acquire(c_dtc, 256 * 8, 8 + N, &slot, d, N, s, &lk,
+                                &capturing, slot_row<N>))
       return rc;
-    (swz ? ks : k)<<<grid, G * TcCfg<N>::T, bytes, s>>>(
-        w, u, g, nelt, sumsq ? geom->workspace : nullptr, umap);
-    dconst_release(3, slot, s, capturing);
+    if (slot == 0)
+      tc2_launch_row<N, G, SGS, KS, N>(sumsq, swz, grid, bytes, w, u, g,
+                                       nelt, geom, umap, s);
+    else
+      tc2_launch_row<N, G, SGS, KS, N + 10>(sumsq, swz, grid, bytes, w, u,
+                                            g, nelt, geom, umap, s);
+    dconst_release(8 + N, slot, s, capturing);
   }
   if (int rc = check_launch("lfb_semlap_f64(dmma2)")) return rc;
   return sumsq ? sem_sumsq_finish(geom->workspace, grid, geom->sumsq, s)
@@ -713,13 +736,13 @@ static int launch_tc(double *w, const double *u, const double *d,
   {
     std::unique_lock<std::mutex> lk;
     bool capturing = false;
-    int slot = N;
-    if (int rc = dconst_acquire(c_dtc, 256 * 8, 3, &slot, d, N, s, &lk,
-                                &capturing))
+    int slot = 0;  // row N: slot 0 of the order's ring (launch_tc2)
+    if (int rc = dconst_acquire(c_dtc, 256 * 8, 8 + N, &slot, d, N, s, &lk,
+                                &capturing, slot_row<N>))
       return rc;
     k<<<grid, G * TcCfg<N>::T, L::total, s>>>(
         w, u, g, nelt, sumsq ? geom->workspace : nullptr);
-    dconst_release(3, slot, s, capturing);
+    dconst_release(8 + N, slot, s, capturing);
   }
   if (int rc = check_launch("lfb_semlap_f64(dmma)")) return rc;
   return sumsq ? sem_sumsq_finish(geom->workspace, grid, geom->sumsq, s)

@@ -231,6 +231,59 @@ def test_semlap_constant_d_slots_across_streams(cuda):
         assert w.cpu().numpy().tobytes() == ref.tobytes()
 
 
+@pytest.mark.parametrize("n,variant", [(8, 50), (8, 0), (12, 50),
+                                       (12, 0), (16, 50), (5, 0)])
+def test_semlap_graph_replay_mixed_with_eager_launches(cuda, n, variant):
+    """a CUDA graph captured with one d, replayed on one
+    stream while eager launches of the same order with other d run on a
+    second stream (and a second graph on a third) -- every kernel reads its
+    d from a constant-bank slot.  Captured launches wait on / record the
+    slot events as graph event nodes, so no slot is overwritten under a
+    running kernel: each result is the oracle's for its own d (bitwise,
+    or within 1e-12 of the summed-term magnitude in DFMA mode)."""
+    nelt = 8192 if n <= 8 else 2048
+    _raw, knl = fx.translate(fx.semlap_source(n))
+    cur = torch.cuda.current_stream(cuda)
+    cases = []
+    for c in range(4):
+        u, d, g = _sem_inputs(n, nelt, cuda, 300 + c)
+        w = torch.full_like(u, float("nan"))
+        env = lfb.env_from_buffers(knl, {"nelt": nelt},
+                                   {"u": u, "d": d, "g": g, "w": w})
+        cases.append((env, u, d, g, w))
+    s_graph, s_eager, s_graph2 = (torch.cuda.Stream(cuda) for _ in range(3))
+    graphs = []
+    for c, s in ((0, s_graph), (2, s_graph2)):
+        L = lfb.Launcher(knl, cases[c][0], variant=variant)
+        L.launch()  # warm up outside the capture
+        torch.cuda.synchronize()
+        gr = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gr, stream=s):
+            L.launch()
+        graphs.append((gr, s))
+    for s in (s_graph, s_eager, s_graph2):
+        s.wait_stream(cur)
+    eager = [lfb.Launcher(knl, cases[c][0], variant=variant) for c in (1, 3)]
+    for rep in range(6):
+        for q, (gr, s) in enumerate(graphs):
+            with torch.cuda.stream(s):
+                gr.replay()
+            with torch.cuda.stream(s_eager):
+                eager[q].launch(stream=s_eager.cuda_stream)
+    torch.cuda.synchronize()
+    for env, u, d, g, w in cases:
+        uh, dh, gh = u.cpu().numpy(), d.cpu().numpy(), g.cpu().numpy()
+        ref = oracle.semlap(np.zeros(nelt * n ** 3), uh, dh, gh, n, nelt,
+                            threads=8)
+        got = w.cpu().numpy()
+        if variant == 0:
+            assert got.tobytes() == ref.tobytes()
+        else:
+            mag = oracle.semlap(np.zeros(nelt * n ** 3), np.abs(uh),
+                                np.abs(dh), np.abs(gh), n, nelt, threads=8)
+            assert (np.abs(got - ref) <= 1e-12 * mag).all()
+
+
 @pytest.mark.parametrize("n", [8, 5])
 def test_semlap_sumsq_epilogue(cuda, n):
     _raw, knl = fx.translate(fx.semlap_source(n))
