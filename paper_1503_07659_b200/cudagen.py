@@ -89,6 +89,27 @@ static __device__ __noinline__ void lfb_oob(long long *err, int insn, int arr,
 }
 """
 
+TRACE_PRELUDE = r"""
+/* write trace (make_env(trace=True), interp.py:79, 381-382): every store
+   appends [insn, array, rank, idx0..4, nv, v0..v11] -- the instruction, the
+   subscript and the values of the inames enclosing the store -- at slot
+   atomicAdd(count); the host sorts the records into the sequential
+   interpreter's order.  tr[0] counts every store, also past the capacity
+   (the host then re-runs with a larger buffer). */
+static __device__ __noinline__ void lfb_trace(long long *tr, i64 cap, int insn,
+    int arr, int rank, i64 i0, i64 i1, i64 i2, i64 i3, i64 i4, int nv,
+    i64 v0, i64 v1, i64 v2, i64 v3, i64 v4, i64 v5, i64 v6, i64 v7, i64 v8,
+    i64 v9, i64 v10, i64 v11) {
+  const unsigned long long s = atomicAdd((unsigned long long *)tr, 1ull);
+  if ((i64)s >= cap) return;
+  long long *r = tr + 8 + 24 * (i64)s;
+  r[0] = insn; r[1] = arr; r[2] = rank;
+  r[3] = i0; r[4] = i1; r[5] = i2; r[6] = i3; r[7] = i4; r[8] = nv;
+  r[9] = v0; r[10] = v1; r[11] = v2; r[12] = v3; r[13] = v4; r[14] = v5;
+  r[15] = v6; r[16] = v7; r[17] = v8; r[18] = v9; r[19] = v10; r[20] = v11;
+}
+"""
+
 TMA_PRELUDE = r"""
 /* precompute footprints by TMA (SURVEY.md §8(f) row 3) */
 struct __align__(64) lfb_tmap { unsigned long long v[16]; };
@@ -248,13 +269,23 @@ class Program:
     checked: str = None     # None, "plain" or "dims"
     insn_ids: tuple = ()    # checked mode: instruction ids by index
     arr_names: tuple = ()   # checked mode: array names by index
+    trace: bool = False     # write-trace build
+    trace_names: tuple = ()  # trace: written names by record id
+    trace_vis: tuple = ()   # trace: per insn index, the inames recorded
 
 
 class _Emitter:
-    def __init__(self, kernel, checked=None):
+    def __init__(self, kernel, checked=None, trace=False):
         k = transforms.expand_all_rules(kernel) if kernel.rules else kernel
         lfk.validate_kernel(k)
         self.k = k
+        # trace: every store also appends a write-trace record; workgroup
+        # temporaries become per-work-item (each work-item then runs the
+        # whole schedule, fetches included, like one iteration of the
+        # reference interpreter's parallel loops, interp.py:385-399)
+        self.trace = trace
+        self.trace_names = []
+        self.trace_vis = {}
         # checked=None: the fast kernel.  "plain" / "dims": every array
         # access checked like the reference's _Evaluator.check_bounds
         # (interp.py:293-308) -- arguments per dimension against the env's
@@ -664,18 +695,51 @@ class _Emitter:
             if self.checked:
                 store_if = self._bounds(insn.lhs)
         val = _cast(rhs, rt, self.dtypes[tgt])
+        tr = self._trace_call(insn) if self.trace else ""
         if store_if is not None:
             # the value first (its loads are checked before the store, the
             # reference's evaluation order), then the checked store
             cond, rec = store_if
             ct = CT[self.dtypes[tgt]]
-            self.line(f"{{ const {ct} lfb_v = {val}; if ({cond}) {lhs} = "
-                      f"lfb_v; else {rec}; }}  /* {insn.id} */")
+            self.line(f"{{ const {ct} lfb_v = {val}; if ({cond}) {{ {lhs} = "
+                      f"lfb_v; {tr}}} else {rec}; }}  /* {insn.id} */")
         else:
             self.line(f"{lhs} = {val};  /* {insn.id} */")
+            if tr:
+                self.line(tr)
         if guarded:
             self.ind -= 1
             self.line("}")
+
+    def _trace_call(self, insn):
+        """The write-trace record of *insn*'s store (interp.py:381-382:
+        (insn id, array, index)) plus the values of the inames visible at
+        the store, from which the host rebuilds the sequential order."""
+        if isinstance(insn.lhs, ex.VarRef):
+            name, idx = insn.lhs.name, []
+        else:
+            name = insn.lhs.array
+            idx = []
+            for ix in insn.lhs.index:
+                aff = ex.expression_to_affine(ix)
+                if aff is not None:
+                    idx.append(f"(i64)({_aff(aff)})")
+                else:
+                    txt, _t = self.rv(ix)
+                    idx.append(f"(i64)({txt})")
+        if len(idx) > 5:
+            raise CodegenError("write trace: arrays of rank > 5")
+        if name not in self.trace_names:
+            self.trace_names.append(name)
+        vis = list(self.visible)
+        if len(vis) > 12:
+            raise CodegenError("write trace: more than 12 enclosing inames")
+        self.trace_vis[self.cur_insn] = tuple(vis)
+        args = ([str(self.cur_insn), str(self.trace_names.index(name)),
+                 str(len(idx))] + idx + ["0"] * (5 - len(idx))
+                + [str(len(vis))] + [f"(i64){v}" for v in vis]
+                + ["0"] * (12 - len(vis)))
+        return f"lfb_trace(lfb_tr, lfb_trcap, {', '.join(args)}); "
 
     def walk(self, node, ctx):
         """ctx: dict(wg=set of shared temporaries, guard='all'|'stmt'|None)"""
@@ -1416,7 +1480,7 @@ class _Emitter:
         wg = {t.name for t in k.temporaries.values()
               if t.address_space == "workgroup" and t.shape}
         shared = set(wg)
-        if wg and not self.plan(wg):
+        if self.trace or (wg and not self.plan(wg)):
             shared = set()
         demoted = wg - shared
         self.visible = list(self.parallel)
@@ -1596,6 +1660,10 @@ class _Emitter:
                 for d in range(len(self.arrays[name])):
                     sig.append(f"i64 lfb_x_{name}_{d}")
                     order.append(f"lfb_x_{name}_{d}")
+        if self.trace:
+            prelude += TRACE_PRELUDE
+            sig += ["long long *lfb_tr", "i64 lfb_trcap"]
+            order += ["lfb_tr", "lfb_trcap"]
         if self.tma_maps:
             sig.append("int lfb_tma")
             order.append("lfb_tma")
@@ -1635,14 +1703,18 @@ class _Emitter:
                        tuple(sorted(shared)), tuple(sorted(demoted)),
                        self.cooperative, key, tuple(self.tma_maps),
                        self.checked, tuple(self.insn_ids),
-                       tuple(self.arr_names))
+                       tuple(self.arr_names), self.trace,
+                       tuple(self.trace_names),
+                       tuple(self.trace_vis.get(q, ())
+                             for q in range(len(self.insn_ids))))
 
 
-def emit_cuda(kernel, checked=None):
+def emit_cuda(kernel, checked=None, trace=False):
     """Render *kernel* (transformed, rules expanded or not) as one CUDA
     kernel; returns a :class:`Program`.  *checked*: None, "plain" (the
-    reference's interpret() checks) or "dims" (interpret_bounds_checked)."""
-    return _Emitter(kernel, checked).emit()
+    reference's interpret() checks) or "dims" (interpret_bounds_checked).
+    *trace*: also record every store (make_env(trace=True))."""
+    return _Emitter(kernel, checked, trace).emit()
 
 
 __all__ = ["Program", "TmaMap", "emit_cuda", "NVRTC_OPTIONS", "promote"]

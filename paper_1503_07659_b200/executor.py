@@ -73,6 +73,9 @@ class DeviceEnv:
     arrays: dict = field(default_factory=dict)   # name -> DeviceArray
     scalars: dict = field(default_factory=dict)  # name -> numpy scalar
     device: torch.device = None
+    # make_env(trace=True): (insn id, name, index) per write, in the
+    # sequential interpreter's order (interp.py:79, 381-382)
+    write_trace: list = None
 
 
 def _device(device):
@@ -95,19 +98,13 @@ def make_device_env(kernel, params, inputs=None, seed=None, trace=False,
     argument order), so a seeded device env holds exactly the values of the
     seeded reference env.
     """
-    if trace:
-        # interp.py:79/381-382 appends (insn, array, index) per write in the
-        # sequential interpreter's order; device work-items write in
-        # parallel, so there is no such order to record
-        raise InterpError("make_env(trace=True) is the sequential "
-                          "interpreter's write trace; the device executor "
-                          "has none (run loopforge.interp for it)")
     dev = _device(device)
     inputs = dict(inputs or {})
     params = {k: int(v) for k, v in params.items()}
     check_assumptions(kernel, params)
     rng = np.random.default_rng(seed) if seed is not None else None
-    env = DeviceEnv(params=params, device=dev)
+    env = DeviceEnv(params=params, device=dev,
+                    write_trace=[] if trace else None)
     for a in kernel.args:
         npt = NP_DTYPE[a.dtype]
         if a.kind == "scalar-value":
@@ -393,6 +390,8 @@ def interpret(kernel, env, bounds_check=False, *, inplace=False, variant=0,
             if a.kind == "global-array" and a.is_output:
                 out.arrays[a.name] = env.arrays[a.name].copy()
                 cloned.append(out.arrays[a.name].data)
+    if env.write_trace is not None:
+        return _interpret_traced(kernel, env, out, bounds_check, stream)
     if stream is not None:
         # the clones above run on the current stream; a launch on another
         # stream must start after them, and the allocator must know the
@@ -415,6 +414,31 @@ def interpret(kernel, env, bounds_check=False, *, inplace=False, variant=0,
     else:
         launcher = make_launcher(kernel, out, variant=variant, engine=engine)
     launcher.launch(stream=stream)
+    return out
+
+
+def _interpret_traced(kernel, env, out, bounds_check, stream):
+    """make_env(trace=True): the trace build of the generated CUDA
+    (cudagen ``trace``) records every store with the values of its
+    enclosing inames; the records are sorted into the reference
+    interpreter's sequential order and appended to a copy of the env's
+    trace (interp.py:66-70, 381-382).  Synchronises: a debugging mode."""
+    from .generic import GenericLauncher, TraceOverflow
+    launcher = GenericLauncher(kernel, out,
+                               checked="dims" if bounds_check else "plain",
+                               trace=True)
+    originals = {n: a.data.clone() for n, a in out.arrays.items()
+                 if any(x.name == n and x.is_output for x in kernel.args)}
+    while True:
+        try:
+            launcher.launch(stream=stream)
+            break
+        except TraceOverflow:
+            # larger buffer (the launcher grew it); outputs back to their
+            # pre-launch values, then run again
+            for n, t in originals.items():
+                out.arrays[n].data.copy_(t)
+    out.write_trace = list(env.write_trace) + launcher.last_trace
     return out
 
 

@@ -23,15 +23,65 @@ _MODULES = {}   # (program key, device index) -> lfb_module handle
 _PROGRAMS = {}  # id(kernel) -> (kernel, Program)
 
 
-def program_for(kernel, checked=None):
-    hit = _PROGRAMS.get((id(kernel), checked))
+def program_for(kernel, checked=None, trace=False):
+    hit = _PROGRAMS.get((id(kernel), checked, trace))
     if hit is not None and hit[0] is kernel:
         return hit[1]
-    prog = emit_cuda(kernel, checked=checked)
+    prog = emit_cuda(kernel, checked=checked, trace=trace)
     if len(_PROGRAMS) > 256:
         _PROGRAMS.clear()
-    _PROGRAMS[(id(kernel), checked)] = (kernel, prog)
+    _PROGRAMS[(id(kernel), checked, trace)] = (kernel, prog)
     return prog
+
+
+class TraceOverflow(Exception):
+    """The write-trace buffer was too small; *needed* records were made."""
+
+    def __init__(self, needed):
+        super().__init__(f"write trace needs {needed} records")
+        self.needed = needed
+
+
+def _schedule_paths(kernel):
+    """insn id -> path through the reference interpreter's schedule tree
+    (codegen.schedule, interp.py:341-363): ('c', child index) per tree level
+    and ('l', iname) per loop, outermost first."""
+    from ._loopforge import codegen, transforms
+    k = transforms.expand_all_rules(kernel) if kernel.rules else kernel
+    paths = {}
+
+    def walk(node, path):
+        for c, child in enumerate(node.children):
+            if isinstance(child, codegen.Statement):
+                paths[child.insn_id] = path + [("c", c)]
+            elif isinstance(child, codegen.Loop):
+                walk(child, path + [("c", c), ("l", child.iname)])
+            else:
+                walk(child, path + [("c", c)])
+
+    walk(codegen.schedule(k), [])
+    return paths, list(codegen.parallel_inames_of(k))
+
+
+def decode_trace(kernel, prog, records):
+    """Device write-trace records -> the reference's ``write_trace`` list of
+    (insn id, name, index tuple), in the sequential interpreter's order:
+    parallel inames outermost in domain order (interp.py:385-399), then the
+    schedule tree's order and loop values (interp.py:341-363)."""
+    paths, parallel = _schedule_paths(kernel)
+    keyed = []
+    for r in records:
+        insn = prog.insn_ids[int(r[0])]
+        name = prog.trace_names[int(r[1])]
+        idx = tuple(int(x) for x in r[3:3 + int(r[2])])
+        vis = prog.trace_vis[int(r[0])]
+        vals = dict(zip(vis, (int(x) for x in r[9:9 + int(r[8])])))
+        key = [vals[p] for p in parallel]
+        for kind, v in paths[insn]:
+            key.append(v if kind == "c" else vals[v])
+        keyed.append((tuple(key), (insn, name, idx)))
+    keyed.sort(key=lambda t: t[0])
+    return [w for _k, w in keyed]
 
 
 def compile_program(prog, narrow=False):
@@ -90,10 +140,12 @@ class GenericLauncher:
     """Prepared launch of the generated kernel (same interface as
     executor.Launcher)."""
 
-    def __init__(self, kernel, env, checked=None):
+    def __init__(self, kernel, env, checked=None, trace=False):
         self.kernel = kernel
         self.env = env
-        self.program = program_for(kernel, checked)
+        self.program = program_for(kernel, checked, trace)
+        self.trace_cap = 1 << 14
+        self.last_trace = None
         self.geometry = launch_geometry(kernel, env.params)
         self._narrow = {}
 
@@ -165,6 +217,8 @@ class GenericLauncher:
             # an empty g.N range: the reference's loop over it runs no
             # iterations (the residual guard omits what launch sizing
             # guarantees, so launching one group anyway would be wrong)
+            if prog.trace:
+                self.last_trace = []
             return
         vals = []
         args = {a.name: a for a in self.kernel.args}
@@ -184,6 +238,16 @@ class GenericLauncher:
                     ext.wait_stream(cur)
                     err.record_stream(ext)
                 vals.append(C.c_void_p(err.data_ptr()))
+            elif name == "lfb_tr":
+                tr = torch.zeros(8 + 24 * self.trace_cap, dtype=torch.int64,
+                                 device=dev)
+                if stream != cur.cuda_stream:
+                    ext = torch.cuda.ExternalStream(stream, device=dev)
+                    ext.wait_stream(cur)
+                    tr.record_stream(ext)
+                vals.append(C.c_void_p(tr.data_ptr()))
+            elif name == "lfb_trcap":
+                vals.append(C.c_int64(self.trace_cap))
             elif name.startswith("lfb_x_"):   # checked mode: env extents
                 arr, d = name[6:].rsplit("_", 1)
                 vals.append(C.c_int64(int(env.arrays[arr].shape[int(d)])))
@@ -209,6 +273,15 @@ class GenericLauncher:
                   f"launch {prog.entry}")
         if prog.checked:
             self._raise_first_oob(err, env)
+        if prog.trace:
+            torch.cuda.synchronize(dev)
+            count = int(tr[0].item())
+            if count > self.trace_cap:
+                self.trace_cap = count
+                raise TraceOverflow(count)
+            recs = tr[8:8 + 24 * count].view(count, 24).cpu().numpy() \
+                if count else []
+            self.last_trace = decode_trace(self.kernel, prog, recs)
 
     def _raise_first_oob(self, err, env):
         """The reference's InterpError for the recorded access

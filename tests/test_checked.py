@@ -7,8 +7,9 @@ detection / sanitizers; the reference's tests/test_interp.py:139-192).
   checked build of the generated CUDA records the first violation of a
   launch (cudagen.py ``checked``), the host raises the reference's message.
 * A read of a temporary no instruction writes raises "never-written".
-* ``make_env(trace=True)``'s sequential write trace has no device analogue:
-  a clear InterpError, not a silently missing attribute.
+* ``make_env(trace=True)``'s write trace: the trace build records every
+  store on the device, the host sorts the records into the sequential
+  interpreter's order -- the same list the reference builds.
 """
 
 import dataclasses
@@ -55,10 +56,17 @@ def test_read_never_written_temporary():
         lfb.interpret(broken, env)
 
 
-def test_trace_has_no_device_analogue():
-    knl = lfk.make_kernel(["{[i]: 0<=i<n}"], "out[i] = 2*a[i]")
-    with pytest.raises(InterpError, match="trace"):
-        lfb.make_device_env(knl, {"n": 4}, trace=True, device="cpu")
+def test_trace_build_compiles():
+    """make_env(trace=True) runs the trace build of the generated CUDA:
+    every store also appends a record; workgroup tiles are per work-item
+    (each work-item runs its own fetch, as in the reference interpreter)."""
+    for src in (fx.gemm_source("f64"), fx.generic_source("cond"),
+                fx.semlap_source(4, block=2)):
+        _raw, knl = fx.translate(src)
+        prog = emit_cuda(knl, checked="plain", trace=True)
+        assert prog.trace and "lfb_trace(" in prog.source
+        assert not prog.shared and not prog.tma
+        assert compile_program(prog, True)[:4] == b"\x7fELF"
 
 
 @pytest.mark.parametrize("mode", ["plain", "dims"])
@@ -206,3 +214,99 @@ def test_side_stream_launch_orders_after_the_clones(cuda):
     env2.arrays["a"].shape = (4,)
     with pytest.raises(InterpError, match="insn_0"):
         lfb.interpret(k2, env2, stream=s)
+
+
+COND_F = """
+subroutine cond(out, inp, n)
+  implicit none
+  real*8 out(n), inp(n)
+  integer n
+
+  do i = 1, n
+    a = inp(i)
+    if (a.ge.3) then
+        b = 2*a
+        do j = 1,3
+            b = 3 * b
+        end do
+        out(i) = 5*b
+    else
+        out(i) = 4*a
+    endif
+  end do
+end
+"""
+
+
+@pytest.mark.gpu
+def test_conditional_write_trace_exactly_one_branch(cuda):
+    """tests/test_interp.py:67-82 restated on the device: every out[i] is
+    written exactly once, by the branch the input selects -- and the whole
+    trace equals the reference interpreter's, order included."""
+    from paper_1503_07659_b200._loopforge import fortran, interp
+    raw, _t, _u = fortran.translate_file_text(COND_F, "cond.f")
+    rng = np.random.default_rng(3)
+    inp = rng.random(8) * 6
+    env = lfb.make_device_env(raw, {"n": 8}, {"inp": inp}, trace=True,
+                              device=cuda)
+    out = lfb.interpret(raw, env)
+    then_id = [i.id for i in raw.instructions
+               if ("loopy_cond0", False) in i.predicates
+               and i.assignee_name() == "out"][0]
+    else_id = [i.id for i in raw.instructions
+               if ("loopy_cond0", True) in i.predicates][0]
+    for i in range(8):
+        writes = [iid for (iid, name, idx) in out.write_trace
+                  if name == "out" and idx == (i,)]
+        assert len(writes) == 1
+        assert writes[0] == (then_id if inp[i] >= 3 else else_id)
+    ref = interp.interpret(raw, interp.make_env(raw, {"n": 8},
+                                                {"inp": inp}, trace=True))
+    assert out.write_trace == ref.write_trace
+    assert lfb.get_output(out, "out").tobytes() == \
+        interp.get_output(ref, "out").tobytes()
+
+
+def _trace_cases():
+    from paper_1503_07659_b200._loopforge import transforms
+    out = []
+    _r, k = fx.translate(fx.gemm_source("f64"))          # workgroup tiles
+    out.append(("dgemm_paper", k, {"m": 20, "n": 12, "l": 40},
+                {"alpha": 0.75}))
+    out.append(("sec51", sec51_precomputed(), {"n": 32}, {}))
+    base = lfk.make_kernel(["{[i]: 0<=i<n}"], "out[i] = 2*a[i]")
+    out.append(("dbl_ragged", transforms.split_iname(
+        base, "i", 8, outer_tag="g.0", inner_tag="l.0"), {"n": 20}, {}))
+    _r, k = fx.translate(fx.semlap_source(4, block=2))
+    out.append(("semlap4", k, {"nelt": 2}, {}))
+    _r, k = fx.translate(fx.generic_source("matvec_acc"))
+    out.append(("mvacc", k, {"n": 16}, {}))
+    knl = lfk.make_kernel(["{[i,j]: 0<=i<3 and 0<=j<5}"],
+                          "out[i] = sum(j, a[i,j])")
+    out.append(("rowsum", knl, {}, {}))
+    return out
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", _trace_cases(), ids=lambda c: c[0])
+def test_write_trace_equals_the_reference(cuda, case):
+    """The device write trace of transformed kernels (work-group tiles,
+    ragged guards, parallel tags, SEM temporaries, reductions) equals the
+    reference interpreter's trace exactly, and a second traced run appends
+    to it (env.copy() keeps the trace, interp.py:66-70)."""
+    from paper_1503_07659_b200._loopforge import interp
+    _name, knl, params, scalars = case
+    ref_env = interp.make_env(knl, params, dict(scalars), seed=5,
+                              trace=True)
+    ref = interp.interpret(knl, ref_env)
+    env = lfb.make_device_env(knl, params, dict(scalars), seed=5,
+                              trace=True, device=cuda)
+    out = lfb.interpret(knl, env)
+    assert out.write_trace == ref.write_trace
+    for a in knl.args:
+        if a.kind == "global-array" and a.is_output:
+            assert lfb.get_output(out, a.name).tobytes() == \
+                interp.get_output(ref, a.name).tobytes()
+    again = lfb.interpret(knl, out)
+    assert again.write_trace == ref.write_trace * 2
+    assert env.write_trace == []
