@@ -69,7 +69,10 @@ inline int dconst_acquire(const T &symbol, size_t slot_bytes, int tag,
                                               cudaEventDisableTiming) !=
                          cudaSuccess)
     return fail(LFB_ERR_LAUNCH, "semlap: event create failed");
-  if (r.used[slot] &&
+  // a captured launch always gets its wait node, also when the slot has
+  // not been used yet: the graph is replayed later, after launches that do
+  // use the slot (an event never recorded waits on nothing)
+  if ((r.used[slot] || *capturing) &&
       cudaStreamWaitEvent(s, r.ev[slot],
                           *capturing ? cudaEventWaitExternal : 0) !=
           cudaSuccess)
