@@ -7,10 +7,11 @@ sm_100a kernels behind a C ABI (include/loopforge_b200.h), and -- for kernels
 outside that set -- with CUDA generated from the kernel's schedule
 (cudagen.py, compiled by NVRTC for sm_100a)::
 
-    from loopforge.fortran import translate_file_text
     import paper_1503_07659_b200 as lfb
 
-    raw, knl, _ = translate_file_text(source)        # unchanged front end
+    # the reference's front end (loopforge.fortran.translate_file_text), with
+    # the paper's alias verbs (add_prefetch, tag_inames, ...) admitted
+    raw, knl, _ = lfb.translate_file_text(source)
     env = lfb.make_device_env(knl, {"nelt": 65536}, seed=0)
     out = lfb.interpret(knl, env)                    # runs on the B200
     w = lfb.get_output(out, "w")
@@ -25,6 +26,8 @@ from .executor import (ENGINES, DeviceArray, DeviceEnv, Launcher,
                        make_device_env, make_launcher, plan_for)
 from .launch import Geometry, launch_geometry
 from .recognize import WORKLOADS, canonicalize, recognize
+from .script import (add_prefetch, assignment_to_subst, fix_parameters,
+                     tag_inames, translate_file_text)
 
 __all__ = [
     "ENGINES", "emit_cuda", "make_launcher",
@@ -33,6 +36,8 @@ __all__ = [
     "interpret_bounds_checked",
     "make_device_env", "plan_for", "Geometry", "launch_geometry",
     "WORKLOADS", "canonicalize", "recognize",
+    "add_prefetch", "assignment_to_subst", "fix_parameters", "tag_inames",
+    "translate_file_text",
 ]
 
 __version__ = "0.1.0"

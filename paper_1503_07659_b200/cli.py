@@ -37,15 +37,15 @@ def _kv(items, what, conv):
 
 
 def _translate(args):
-    from ._loopforge import fortran
+    from . import script
     with open(args.file) as f:
         src = f.read()
     extra = ()
     if args.transforms:
         with open(args.transforms) as f:
             extra = (f.read(),)
-    raw, knl, _unit = fortran.translate_file_text(src, args.file,
-                                                  extra_scripts=extra)
+    raw, knl, _unit = script.translate_file_text(src, args.file,
+                                                 extra_scripts=extra)
     return raw, knl
 
 

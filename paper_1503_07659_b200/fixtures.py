@@ -194,9 +194,11 @@ end subroutine
 
 
 def translate(source, name="<fixture>"):
-    """(raw, transformed) kernels via the reference front end."""
-    from ._loopforge import fortran
-    raw, transformed, _unit = fortran.translate_file_text(source, name)
+    """(raw, transformed) kernels via the reference front end (its parser,
+    lowering and transform verbs; script.py admits the paper's alias verbs
+    as well, lowered to the reference's)."""
+    from .script import translate_file_text
+    raw, transformed, _unit = translate_file_text(source, name)
     return raw, transformed
 
 
