@@ -136,8 +136,11 @@ int64_t lfb_sgemm_workspace(int l, int m, int n);
 
 /* dgemm: the same kernel in real*8 -- the reference's own DGEMM test
  * (tests/test_fortran.py:72-103)
- *                                       emitted: void dgemm(int m, int n, int l, double alpha, double const *a, double const *b, double *c)
- * (argument order here is the sgemm entry's).  geom->variant: 0 the FP64
+ * emitted (codegen.py:511-527: kernel.args in declaration order, then the
+ * remaining params sorted by name):
+ *   void dgemm(double alpha, double const *a, double const *b, double *c,
+ *              int l, int m, int n)
+ * -- the same order as this entry.  geom->variant: 0 the FP64
  * tensor cores (DMMA; tolerance parity, fp64 within 1e-12) when m % 128,
  * n % 128, l % 16 == 0 and a, b are 16-byte aligned, else the bit-exact
  * CUDA-core kernel; 1 bit-exact; 2 tensor cores only                     */
