@@ -121,6 +121,23 @@ int lfb_semlap_f64(double *w, const double *u, const double *d,
 /* doubles of workspace lfb_semlap_f64 needs when geom->sumsq != NULL */
 int64_t lfb_semlap_workspace(int npts, int nelt, const lfb_launch *geom);
 
+/* dssum: SEM direct-stiffness summation Q Q^T on element-local w (the
+ * semlap layout) over a structured box of ex x ey x ez elements of n points
+ * per direction -- SURVEY.md §8(f) row 4, not a reference entry point (the
+ * reference operator is element-local, interp.py:385-399; this is the
+ * assembly step an SEM solver applies after it).  Global nodes with
+ * zlo <= Z <= zhi (Z = ez_elem (n-1) + k).  mode 0: every node shared by
+ * 2/4/8 elements gets the sum of its copies, formed left to right in
+ * ascending element order; 1: that sum into plane_out[X + (ex(n-1)+1) Y],
+ * no write-back (a rank's top interface plane); 2: start from plane_in, add
+ * the copies, write back and into plane_out (the upper rank of an
+ * interface); 3: write plane_in into the copies.  Modes 1-3 take one
+ * element plane (zlo == zhi, a multiple of n-1).  Deterministic; bitwise
+ * the single-domain result when the ranks chain modes 1 -> 2 -> 3. */
+int lfb_dssum_f64(double *w, int n, int ex, int ey, int ez, int zlo,
+                  int zhi, int mode, const double *plane_in,
+                  double *plane_out, lfb_stream stream);
+
 /* sgemm: c[i,j] = c[i,j] + alpha*b[k,j]*a[i,k] over ascending k, all
  * column major: a (m,l), b (l,n), c (m,n)
  *                                       emitted: void sgemm(float alpha, float const *a, float const *b, float *c, int l, int m, int n)

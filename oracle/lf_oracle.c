@@ -121,3 +121,66 @@ double lfo_sumsq_f64(const double *w, int64_t n) {
   for (int64_t q = 0; q < n; ++q) s = s + w[q] * w[q];
   return s;
 }
+
+/* SEM direct-stiffness summation (gather-scatter, Q Q^T) on a structured
+ * box of Ex x Ey x Ez elements of n points per direction (SURVEY.md §8(f)
+ * row 4 -- not in the reference, whose operator is element-local; this is
+ * the oracle of paper_1503_07659_b200/csrc/dssum.cu, same order of
+ * operations).  Element e = ex + Ex (ey + Ey ez), local node (i, j, k) at
+ * w[i + n j + n^2 k + n^3 e] (the semlap layout); global node
+ * (X, Y, Z) = (ex p + i, ey p + j, ez p + k), p = n - 1.  A node on an
+ * element boundary has 2, 4 or 8 local copies; their sum is formed left
+ * to right in ascending element order and written back to every copy.
+ * Nodes with zlo <= Z <= zhi only; mode 0 sum + write back, 1 sum into
+ * plane_out[X + (Ex p + 1) Y] (partial of a rank's top interface), 2 start
+ * from plane_in, add the copies, write back and to plane_out (the upper
+ * rank of an interface), 3 write plane_in to the copies. */
+static int64_t lfo_cands(int64_t X, int64_t p, int64_t E, int64_t *el,
+                         int64_t *loc) {
+  const int64_t q = X / p, r = X % p;
+  if (r == 0 && q > 0 && q < E) {
+    el[0] = q - 1, loc[0] = p;
+    el[1] = q, loc[1] = 0;
+    return 2;
+  }
+  el[0] = q < E ? q : E - 1;
+  loc[0] = X - el[0] * p;
+  return 1;
+}
+
+void lfo_dssum_f64(double *w, int64_t n, int64_t Ex, int64_t Ey, int64_t Ez,
+                   int64_t zlo, int64_t zhi, int64_t mode,
+                   const double *plane_in, double *plane_out) {
+  const int64_t p = n - 1, GX = Ex * p + 1, GY = Ey * p + 1;
+  const int64_t n3 = n * n * n;
+  for (int64_t Z = zlo; Z <= zhi; ++Z)
+    for (int64_t Y = 0; Y < GY; ++Y)
+      for (int64_t X = 0; X < GX; ++X) {
+        if (mode == 0 && X % p && Y % p && Z % p) continue;  /* unique */
+        int64_t ex[2], ey[2], ez[2], li[2], lj[2], lk[2];
+        const int64_t nx = lfo_cands(X, p, Ex, ex, li);
+        const int64_t ny = lfo_cands(Y, p, Ey, ey, lj);
+        const int64_t nz = lfo_cands(Z, p, Ez, ez, lk);
+        int64_t off[8];
+        int64_t c = 0;
+        for (int64_t a = 0; a < nz; ++a)      /* ascending element index */
+          for (int64_t b = 0; b < ny; ++b)
+            for (int64_t f = 0; f < nx; ++f)
+              off[c++] = li[f] + n * lj[b] + n * n * lk[a] +
+                         n3 * (ex[f] + Ex * (ey[b] + Ey * ez[a]));
+        const int64_t pl = X + GX * Y;
+        double s;
+        int64_t q0 = 0;
+        if (mode == 2 || mode == 3) {
+          s = plane_in[pl];
+        } else {
+          s = w[off[0]];
+          q0 = 1;
+        }
+        if (mode != 3)
+          for (int64_t q = q0; q < c; ++q) s = s + w[off[q]];
+        if (mode == 1 || mode == 2) plane_out[pl] = s;
+        if (mode != 1)
+          for (int64_t q = 0; q < c; ++q) w[off[q]] = s;
+      }
+}

@@ -59,6 +59,7 @@ def lib():
             "lfo_sgemm_f32": [F, P, P, P, I64, I64, I64, I64, I64],
             "lfo_dgemm_f64": [D, P, P, P, I64, I64, I64, I64, I64],
             "lfo_sumsq_f64": [P, I64],
+            "lfo_dssum_f64": [P, I64, I64, I64, I64, I64, I64, I64, P, P],
         }
         for name, args in sig.items():
             getattr(L, name).argtypes = args
@@ -119,6 +120,18 @@ def sgemm(alpha, a, b, c, l, m, n, cols=None, threads=1):
     _parallel(lambda j0, j1: f(alpha, _p(a), _p(b), _p(c), l, m, n, j0, j1),
               lo, hi, threads)
     return c
+
+
+def dssum(w, n, ex, ey, ez, zlo=0, zhi=None, mode=0, plane_in=None,
+          plane_out=None):
+    """Q Q^T on element-local w (lf_oracle.c lfo_dssum_f64), in place."""
+    p = n - 1
+    if zhi is None:
+        zhi = ez * p
+    lib().lfo_dssum_f64(_p(w), n, ex, ey, ez, zlo, zhi, mode,
+                        None if plane_in is None else _p(plane_in),
+                        None if plane_out is None else _p(plane_out))
+    return w
 
 
 def sumsq(w):

@@ -53,6 +53,7 @@ SIGNATURES = {
     "lfb_matvec_f64": [P, P, P, I32, LP, P],
     "lfb_semlap_f64": [P, P, P, P, I32, LP, P],
     "lfb_semlap_workspace": [I32, I32, LP],
+    "lfb_dssum_f64": [P, I32, I32, I32, I32, I32, I32, I32, P, P, P],
     "lfb_sgemm_f32": [F, P, P, P, I32, I32, I32, LP, P],
     "lfb_sgemm_workspace": [I32, I32, I32],
     "lfb_dgemm_f64": [D, P, P, P, I32, I32, I32, LP, P],
