@@ -1098,9 +1098,73 @@ def bench_workload(wl, args, local, cpu=True):
                 "config": {"workload": "semlap orders 3..15, nelt = "
                                        "2^25/n^3 (~2 GiB traffic each)"}}
 
+    if wl == "semop":
+        return semop_bench(args, 0, 1, local, e=args.semop_e or 64)
     if wl == "generic":
         return generic_bench(args, local)
     raise SystemExit(f"unknown workload {wl}")
+
+
+def semop_bench(args, rank, world, local, e=128, n=8):
+    """The assembled SEM operator w <- Q Q^T semlap(u) on a box of e^3
+    elements: the element-local operator (DFMA
+    mode, the headline kernel) followed by the direct-stiffness summation
+    (csrc/dssum.cu).  Ranks own slabs of element layers; the interface
+    planes go through the bitwise partial -> continue -> write-back protocol
+    over NCCL point-to-point (assembly.dssum_sharded).  value = whole-job
+    GDOF/s of the assembled operator; the dssum kernel's own time and
+    bandwidth (algorithmic bytes: every local copy of a shared node read
+    and written once, 16 (n^3 - (n-2)^3) B per element) beside it."""
+    import torch
+
+    import paper_1503_07659_b200 as lfb
+    from paper_1503_07659_b200 import fixtures as fx
+    from paper_1503_07659_b200.assembly import BoxMesh, dssum_sharded
+    dev = torch.device("cuda", local)
+    mesh = BoxMesh(e, e, e, n)
+    slab = mesh.slab(rank, world)
+    _r, knl = fx.translate(fx.semlap_source(n), "semlap.f")
+    u, d, g, w = sem_buffers(n, slab.nelt, dev, 500 + rank)
+    env = lfb.env_from_buffers(knl, {"nelt": slab.nelt},
+                               {"u": u, "d": d, "g": g, "w": w})
+    L = lfb.Launcher(knl, env, variant=50)
+
+    def step():
+        L.launch()
+        dssum_sharded(w, mesh, rank, world)
+
+    ms, ms_local, clocks = timed(step, args.steps, args.warmup, world,
+                                 local)
+    ms_ds, ms_ds_local, _c = timed(lambda: dssum_sharded(w, mesh, rank,
+                                                         world),
+                                   args.steps, args.warmup, world, local)
+    peak, peak_src = _peaks()
+    ds_bytes = 16 * (n ** 3 - (n - 2) ** 3) * slab.nelt
+    res = {"metric": "assembled SEM operator (semlap + Q Q^T) GDOF/s",
+           "value": mesh.nelt * n ** 3 / (ms * 1e-3) / 1e9,
+           "unit": "GDOF/s", "ms_per_step": ms, "dtype": "f64",
+           "n_gpus": world, "scaling": "strong",
+           "config": {"workload": f"box of {e}^3 elements, order {n - 1}, "
+                                  "semlap (DFMA mode) + direct-stiffness "
+                                  "summation; element layers sharded over "
+                                  f"{world} rank(s)",
+                      "mesh": [e, e, e, n], "nelt": mesh.nelt},
+           "dssum": {"ms_per_step": ms_ds,
+                     "share_of_step": ms_ds / ms,
+                     "roofline": {"bound": "hbm",
+                                  "achieved": ds_bytes
+                                  / (ms_ds_local * 1e-3) / 1e9,
+                                  "peak": peak, "unit": "GB/s",
+                                  "frac": ds_bytes / (ms_ds_local * 1e-3)
+                                  / 1e9 / peak,
+                                  "peak_source": peak_src,
+                                  "algorithmic_bytes_per_launch": ds_bytes},
+                     "exchange": "none" if world == 1 else
+                     "2 plane exchanges per interface (NCCL P2P)"},
+           "clocks": clocks}
+    del env, L, u, d, g, w
+    torch.cuda.empty_cache()
+    return res
 
 
 def generic_bench(args, local):
@@ -1182,7 +1246,7 @@ def generic_bench(args, local):
 
 
 CONFIG_WORKLOADS = ("fill", "axpy", "matvec", "sem65k", "sgemm", "dgemm",
-                    "sweep")
+                    "sweep", "semop")
 
 
 def configs_bench(args, local):
@@ -1318,6 +1382,9 @@ def main():
                     help="skip the other BASELINE configs in the default "
                          "line")
     ap.add_argument("--e2e-nelt", type=int, default=0)
+    ap.add_argument("--semop-e", type=int, default=0,
+                    help="elements per direction of the semop box (default "
+                         "64 in the configs line, 128 for --workload semop)")
     ap.add_argument("--e2e-chunk", type=int, default=1 << 17,
                     help="elements per host<->device chunk in the e2e run")
     args = ap.parse_args()
@@ -1364,6 +1431,17 @@ def main():
 
     rank, world, local = dist_init(args.gpus)
     import torch
+    if args.workload == "semop":
+        res = semop_bench(args, rank, world, local, e=args.semop_e or 128)
+        res.update({"steps": args.steps, "warmup": args.warmup,
+                    "higher_is_better": True, "vs_baseline": None,
+                    "data": "synthetic", "comm": comm_report(world, local)})
+        if rank == 0:
+            print(json.dumps(res))
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+        return
     if args.workload not in ("sem2m", "sem65k"):
         if rank == 0:
             print(json.dumps(bench_workload(args.workload, args, local,

@@ -159,3 +159,25 @@ def test_bench_refuses_more_gpus_than_visible():
     d = json.loads([l for l in r.stdout.splitlines()
                     if l.startswith("{")][0])
     assert "only" in d["error"]
+
+
+@pytest.mark.gpu
+def test_bench_semop_two_ranks(tmp_path):
+    """The assembled operator (semlap + Q Q^T) with its interface exchange
+    on 2 ranks (both on cuda:0, gloo): one JSON line, n_gpus 2."""
+    import json
+    import subprocess
+    import sys
+    env = dict(os.environ, LFB_BENCH_ONE_DEVICE="1", LFB_BENCH_BACKEND="gloo")
+    env.pop("WORLD_SIZE", None)
+    r = subprocess.run(
+        [sys.executable, os.path.join(REPO, "bench.py"), "--gpus", "2",
+         "--workload", "semop", "--semop-e", "16", "--steps", "3",
+         "--warmup", "3"],
+        capture_output=True, text=True, timeout=900, env=env, cwd=REPO)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0
+    assert d["comm"]["world_size"] == 2
