@@ -8,13 +8,12 @@
 // direction (p = n - 1), element e = ex + Ex (ey + Ey ez), local node
 // (i, j, k) at w[i + n j + n^2 k + n^3 e] (the semlap layout), global node
 // (X, Y, Z) = (ex p + i, ey p + j, ez p + k).  A node on an element face /
-// edge / corner has 2 / 4 / 8 local copies.  One thread per global node in
-// the requested Z range (grid-stride, 64-bit): the copies are summed left to
-// right in ascending element order -- a fixed order, so the result is
-// deterministic and bitwise the oracle's (oracle/lf_oracle.c
-// lfo_dssum_f64) -- and the sum is written back to every copy.  Interior
-// nodes (one copy) are not touched.  Warps walk X fastest: consecutive lanes
-// hit consecutive i of the same element, so every copy access is coalesced.
+// edge / corner has 2 / 4 / 8 local copies.  One thread per shared global
+// node of the requested Z range: the copies are summed left to right in
+// ascending element order -- a fixed order, so the result is deterministic
+// and bitwise the oracle's (oracle/lf_oracle.c lfo_dssum_f64) -- and the
+// sum is written back to every copy.  Interior nodes (one copy) are not
+// touched.  CTAs walk rows of global nodes (see dssum_kernel).
 //
 // Multi-GPU (paper_1503_07659_b200/assembly.py): ranks own slabs of element
 // layers in z; an interface plane's sum must be the single-GPU sum, so the
@@ -26,17 +25,72 @@
 
 namespace lfb {
 
-__device__ __forceinline__ int cands(int64_t X, int p, int E, int *el,
-                                     int *loc) {
+// the elements along one direction holding global coordinate X, and the
+// local index in each: two (lower first) on an interior element plane, else
+// one (then slot 1 repeats slot 0)
+__device__ __forceinline__ int cands(int64_t X, int p, int E, int &el0,
+                                     int &loc0, int &el1, int &loc1) {
   const int64_t q = X / p, r = X - q * p;
   if (r == 0 && q > 0 && q < E) {
-    el[0] = (int)q - 1, loc[0] = p;
-    el[1] = (int)q, loc[1] = 0;
+    el0 = (int)q - 1, loc0 = p, el1 = (int)q, loc1 = 0;
     return 2;
   }
-  el[0] = q < E ? (int)q : E - 1;
-  loc[0] = (int)(X - (int64_t)el[0] * p);
+  el0 = q < E ? (int)q : E - 1;
+  loc0 = (int)(X - (int64_t)el0 * p);
+  el1 = el0, loc1 = loc0;
   return 1;
+}
+
+// one CTA per row (Y, Z) of global nodes, threads over X (uniform per
+// CTA, so no divergence between "full" and "sparse" rows and no 64-bit
+// division per node).  A row with Y or Z on an element plane is full: every
+// node may be shared, consecutive X are consecutive i of one element
+// (coalesced).  Otherwise only the nodes on x-element planes are shared
+// (X = ex p, two copies): a sparse row has Ex + 1 candidates.
+template <int MODE>
+__device__ __forceinline__ void dssum_node(double *__restrict__ w, int n,
+                                           int p, int Ex, int Ey, int Ez,
+                                           int64_t X, int64_t Y, int64_t Z,
+                                           int64_t pl,
+                                           const double *__restrict__ pin,
+                                           double *__restrict__ pout) {
+  const int64_t n2 = (int64_t)n * n, n3 = n2 * n;
+  int ex[2], ey[2], ez[2], li[2], lj[2], lk[2];
+  const int nx = cands(X, p, Ex, ex[0], li[0], ex[1], li[1]);
+  const int ny = cands(Y, p, Ey, ey[0], lj[0], ey[1], lj[1]);
+  const int nz = cands(Z, p, Ez, ez[0], lk[0], ez[1], lk[1]);
+  if (MODE == 0 && nx * ny * nz == 1) return;  // one copy: nothing to do
+  // copy (a, b, f) at fixed slot 4a + 2b + f: lexicographic = ascending
+  // element index; fully unrolled and predicated (no local-memory array)
+  int64_t off[8];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b)
+#pragma unroll
+      for (int f = 0; f < 2; ++f)
+        off[4 * a + 2 * b + f] =
+            li[f] + n * lj[b] + n2 * lk[a] +
+            n3 * (ex[f] + (int64_t)Ex * (ey[b] + (int64_t)Ey * ez[a]));
+  double s = 0.0;
+  bool first = !(MODE == 2 || MODE == 3);
+  if (!first) s = pin[pl];
+  if (MODE != 3) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      if ((q >> 2) < nz && ((q >> 1) & 1) < ny && (q & 1) < nx) {
+        const double v = w[off[q]];
+        s = first ? v : dadd(s, v);
+        first = false;
+      }
+    }
+  }
+  if (MODE == 1 || MODE == 2) pout[pl] = s;
+  if (MODE != 1) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if ((q >> 2) < nz && ((q >> 1) & 1) < ny && (q & 1) < nx) w[off[q]] = s;
+  }
 }
 
 template <int MODE>
@@ -46,45 +100,20 @@ __global__ void __launch_bounds__(256)
                  double *__restrict__ plane_out) {
   const int p = n - 1;
   const int64_t GX = (int64_t)Ex * p + 1, GY = (int64_t)Ey * p + 1;
-  const int64_t total = GX * GY * (int64_t)(zhi - zlo + 1);
-  const int64_t n2 = (int64_t)n * n, n3 = n2 * n;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-       t < total; t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t X = t % GX;
-    const int64_t r = t / GX;
-    const int64_t Y = r % GY;
-    const int64_t Z = zlo + r / GY;
-    if (MODE == 0 && (X % p) && (Y % p) && (Z % p)) continue;  // unique
-    int ex[2], ey[2], ez[2], li[2], lj[2], lk[2];
-    const int nx = cands(X, p, Ex, ex, li);
-    const int ny = cands(Y, p, Ey, ey, lj);
-    const int nz = cands(Z, p, Ez, ez, lk);
-    int64_t off[8];
-    int c = 0;
-#pragma unroll
-    for (int a = 0; a < 2; ++a)
-#pragma unroll
-      for (int b = 0; b < 2; ++b)
-#pragma unroll
-        for (int f = 0; f < 2; ++f)
-          if (a < nz && b < ny && f < nx)
-            off[c++] = li[f] + n * lj[b] + n2 * lk[a] +
-                       n3 * (ex[f] + (int64_t)Ex * (ey[b] +
-                                                    (int64_t)Ey * ez[a]));
-    const int64_t pl = X + GX * Y;
-    double s;
-    int q0 = 0;
-    if (MODE == 2 || MODE == 3) {
-      s = plane_in[pl];
+  const int64_t rows = GY * (int64_t)(zhi - zlo + 1);
+  for (int64_t row = blockIdx.x; row < rows; row += gridDim.x) {
+    const int64_t Y = row % GY;
+    const int64_t Z = zlo + row / GY;
+    const bool full = MODE != 0 || Y % p == 0 || Z % p == 0;
+    if (full) {
+      for (int64_t X = threadIdx.x; X < GX; X += blockDim.x)
+        dssum_node<MODE>(w, n, p, Ex, Ey, Ez, X, Y, Z, X + GX * Y, plane_in,
+                         plane_out);
     } else {
-      s = w[off[0]];
-      q0 = 1;
+      for (int64_t q = threadIdx.x + 1; q < Ex; q += blockDim.x)
+        dssum_node<MODE>(w, n, p, Ex, Ey, Ez, q * p, Y, Z, q * p + GX * Y,
+                         plane_in, plane_out);
     }
-    if (MODE != 3)
-      for (int q = q0; q < c; ++q) s = dadd(s, w[off[q]]);
-    if (MODE == 1 || MODE == 2) plane_out[pl] = s;
-    if (MODE != 1)
-      for (int q = 0; q < c; ++q) w[off[q]] = s;
   }
 }
 
@@ -111,12 +140,11 @@ extern "C" int lfb_dssum_f64(double *w, int n, int ex, int ey, int ez,
   if (!w || ((mode == 2 || mode == 3) && !plane_in) ||
       ((mode == 1 || mode == 2) && !plane_out))
     return fail(LFB_ERR_ARG, "lfb_dssum_f64: null buffer");
-  const int64_t total = ((int64_t)ex * (n - 1) + 1) *
-                        ((int64_t)ey * (n - 1) + 1) * (zhi - zlo + 1);
+  const int64_t rows = ((int64_t)ey * (n - 1) + 1) * (zhi - zlo + 1);
   int sms = sm_count(nullptr);
   if (sms <= 0) sms = 148;
-  int64_t blocks = (total + 255) / 256;
-  if (blocks > (int64_t)sms * 8) blocks = (int64_t)sms * 8;
+  int64_t blocks = rows;
+  if (blocks > (int64_t)sms * 32) blocks = (int64_t)sms * 32;
   if (blocks < 1) blocks = 1;
   cudaStream_t s = (cudaStream_t)stream;
   switch (mode) {
