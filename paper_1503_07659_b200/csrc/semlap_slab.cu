@@ -272,235 +272,7 @@ __global__ void __launch_bounds__(G *SlabCfg<N>::T, 1)
   if constexpr (SUMSQ) block_sumsq_partial(acc, partials);
 }
 
-// The same data flow with the loops turned inside out: l outermost, the
-// slices (phase 1: the KS slices of a slab step; phase 2: all n outputs of
-// the column) innermost.  Every accumulation chain still runs l ascending
-// with the reference's operation order, but the chains of different k now
-// advance in lockstep, so each thread has 3 KS (phase 1) or n (phase 2)
-// independent chains in flight instead of one long dependent chain at a
-// time -- the FP64 pipe's 8-cycle DADD latency is covered by the thread's
-// own ILP rather than by more warps, which the smem of a high-order element
-// does not allow.
-template <int N, int G, int SGS, int KS, bool DREG, bool SUMSQ, bool F>
-__global__ void __launch_bounds__(G *SlabCfg<N>::T, 1)
-    semlap_slab2_kernel(double *__restrict__ w, const double *__restrict__ u,
-                        const double *__restrict__ d,
-                        const double *__restrict__ g, int64_t nelt,
-                        double *__restrict__ partials) {
-  using C = SlabCfg<N>;
-  using L = SlabSmem<N, G, SGS, KS>;
-  constexpr int NP = C::NP, N2 = C::N2, T = C::T, R = C::R;
-  constexpr int STEPS = (N + KS - 1) / KS;
-  static_assert(G * (2 + SGS) <= 32, "too many mbarriers");
-
-  extern __shared__ __align__(128) unsigned char smem[];
-  uint64_t *bars = reinterpret_cast<uint64_t *>(smem);
-  double *dn = reinterpret_cast<double *>(smem + L::d_off);
-  double *dt = dn + N2;
-
-  const int tid = threadIdx.x;
-  const int grp = tid / T;
-  const int lt = tid % T;
-  const int i = lt % N;
-  const int j = lt / N;
-  const bool active = lt < N2;
-
-  unsigned char *gbase = smem + L::grp_off + (size_t)grp * L::grp_bytes;
-  double *ustage = reinterpret_cast<double *>(gbase);
-  double *slabs = ustage + 2 * C::UST;
-  double *scr_r = slabs + SGS * KS * C::SLAB;
-  double *scr_s = scr_r + C::SCR;
-  uint64_t *ubar = bars + grp * (2 + SGS);
-  uint64_t *gbar = ubar + 2;
-
-  const int64_t q0 = (int64_t)blockIdx.x * G + grp;
-  const int64_t Q = (int64_t)gridDim.x * G;
-  const int64_t mine = nelt > q0 ? (nelt - q0 + Q - 1) / Q : 0;
-  auto elem = [&](int64_t m) -> int64_t { return q0 + m * Q; };
-
-  if (tid == 0) {
-    for (int q = 0; q < G * (2 + SGS); ++q) mbar_init(&bars[q], 1);
-    fence_mbar_init();
-  }
-  __syncthreads();
-
-  const uint64_t pol = policy_evict_first();
-  const int64_t u_bytes_total = nelt * NP * 8;
-  auto u_lead = [&](int64_t e) -> int { return (int)((e * NP) & 1); };
-  auto u_span = [&](int64_t e) -> int64_t {
-    return ((int64_t)(u_lead(e) + NP) * 8 + 15) / 16 * 16;
-  };
-  auto u_bulk_ok = [&](int64_t e) -> bool {
-    return (e * NP - u_lead(e)) * 8 + u_span(e) <= u_bytes_total;
-  };
-  auto issue_u = [&](int64_t m) {
-    const int64_t e = elem(m);
-    const int st = (int)(m & 1);
-    if (u_bulk_ok(e)) {
-      mbar_arrive_expect_tx(&ubar[st], (uint32_t)u_span(e));
-      bulk_g2s_stream(ustage + st * C::UST, u + e * NP - u_lead(e),
-                      (uint32_t)u_span(e), &ubar[st], pol);
-    } else {
-      mbar_arrive_expect_tx(&ubar[st], 0);
-    }
-  };
-  auto issue_slab = [&](int64_t q) {
-    const int64_t m = q / STEPS;
-    const int step = (int)(q % STEPS);
-    const int k0 = step * KS;
-    const int nk = (N - k0) < KS ? (N - k0) : KS;
-    const int64_t e = elem(m);
-    const int slot = (int)(q % SGS);
-    mbar_arrive_expect_tx(&gbar[slot], (uint32_t)(nk * C::SLAB * 8));
-    bulk_g2s_stream(slabs + (size_t)slot * KS * C::SLAB,
-                    g + e * 6 * NP + (int64_t)k0 * 6 * N2, nk * C::SLAB * 8,
-                    &gbar[slot], pol);
-  };
-
-  const int64_t nsteps = mine * STEPS;
-  if (lt == 0) {
-    for (int64_t m = 0; m < 2 && m < mine; ++m) issue_u(m);
-    for (int64_t q = 0; q < SGS && q < nsteps; ++q) issue_slab(q);
-  }
-  for (int q = tid; q < N2; q += G * T) {
-    const double v = d[q];
-    dn[q] = v;
-    dt[(q / N) + N * (q % N)] = v;
-  }
-  __syncthreads();
-
-  double acc = 0.0;
-  for (int64_t m = 0; m < mine; ++m) {
-    const int64_t e = elem(m);
-    const int st = (int)(m & 1);
-    mbar_wait(&ubar[st], (uint32_t)((m >> 1) & 1));
-    const double *su = ustage + st * C::UST + u_lead(e);
-    if (!u_bulk_ok(e)) {
-      double *dst = ustage + st * C::UST + u_lead(e);
-      for (int q = lt; q < NP; q += T) dst[q] = u[e * NP + q];
-      named_bar_sync(1 + grp, T);
-    }
-
-    double wt[N];
-    double ucol[N];
-    double da[N], db[N];
-    if (active) {
-#pragma unroll
-      for (int l = 0; l < N; ++l) ucol[l] = su[i + N * j + N2 * l];
-      if constexpr (DREG) {
-#pragma unroll
-        for (int l = 0; l < N; ++l) da[l] = dn[i + N * l], db[l] = dn[j + N * l];
-      }
-    }
-#pragma unroll
-    for (int step = 0; step < STEPS; ++step) {
-      const int64_t q = m * STEPS + step;
-      const int slot = (int)(q % SGS);
-      mbar_wait(&gbar[slot], (uint32_t)((q / SGS) & 1));
-      if (active) {
-        const double *gs = slabs + (size_t)slot * KS * C::SLAB;
-        double ur[KS], us[KS], ut[KS];
-#pragma unroll
-        for (int kk = 0; kk < KS; ++kk) ur[kk] = us[kk] = ut[kk] = 0.0;
-#pragma unroll
-        for (int l = 0; l < N; l += 2) {
-#pragma unroll
-          for (int h = 0; h < 2 && l + h < N; ++h) {
-            const int ll = l + h;
-            const double a = DREG ? da[ll] : dn[i + N * ll];
-            const double b = DREG ? db[ll] : dn[j + N * ll];
-#pragma unroll
-            for (int kk = 0; kk < KS; ++kk) {
-              const int k = step * KS + kk;
-              if (k < N) {
-                const double *row = su + N * j + N2 * k;
-                const double *col = su + i + N2 * k;
-                ur[kk] = mac<F>(ur[kk], a, row[ll]);
-                us[kk] = mac<F>(us[kk], b, col[N * ll]);
-                ut[kk] = mac<F>(ut[kk], c_dslab[N][k + N * ll], ucol[ll]);
-              }
-            }
-          }
-        }
-#pragma unroll
-        for (int kk = 0; kk < KS; ++kk) {
-          const int k = step * KS + kk;
-          if (k < N) {
-            const double *gp = gs + kk * C::SLAB + 6 * (i + N * j);
-            const double2 g01 = *reinterpret_cast<const double2 *>(gp);
-            const double2 g23 = *reinterpret_cast<const double2 *>(gp + 2);
-            const double2 g45 = *reinterpret_cast<const double2 *>(gp + 4);
-            scr_r[i + R * j + R * N * k] =
-                comb3<F>(g01.x, ur[kk], g01.y, us[kk], g23.x, ut[kk]);
-            scr_s[j + R * i + R * N * k] =
-                comb3<F>(g01.y, ur[kk], g23.y, us[kk], g45.x, ut[kk]);
-            wt[k] = comb3<F>(g23.x, ur[kk], g45.x, us[kk], g45.y, ut[kk]);
-          }
-        }
-      }
-      named_bar_sync(1 + grp, T);
-      if (lt == 0) {
-        if (q + SGS < nsteps) {
-          fence_proxy_async_smem();
-          issue_slab(q + SGS);
-        }
-        if (step == STEPS - 1 && m + 2 < mine) {
-          fence_proxy_async_smem();
-          issue_u(m + 2);
-        }
-      }
-    }
-
-    if (active) {
-      if constexpr (DREG) {
-#pragma unroll
-        for (int l = 0; l < N; ++l) da[l] = dt[i + N * l], db[l] = dt[j + N * l];
-      }
-      double s[N];
-#pragma unroll
-      for (int k = 0; k < N; ++k) s[k] = 0.0;
-#pragma unroll
-      for (int l = 0; l < N; l += 2) {
-        double a0 = DREG ? da[l] : dt[i + N * l];
-        double b0 = DREG ? db[l] : dt[j + N * l];
-        double a1 = 0.0, b1 = 0.0;
-        if (l + 1 < N) {
-          a1 = DREG ? da[l + 1] : dt[i + N * (l + 1)];
-          b1 = DREG ? db[l + 1] : dt[j + N * (l + 1)];
-        }
-#pragma unroll
-        for (int k = 0; k < N; ++k) {
-          // wr(l.., j, k) row pair; ws stored transposed: ws(i, l.., k)
-          // is the contiguous pair at scr_s[l + R i + R N k]
-          double r0, r1 = 0.0, s0, s1 = 0.0;
-          if (l + 1 < N) {
-            slab_pair<N>(scr_r + l + R * j + R * N * k, r0, r1);
-            slab_pair<N>(scr_s + l + R * i + R * N * k, s0, s1);
-          } else {
-            r0 = scr_r[l + R * j + R * N * k];
-            s0 = scr_s[l + R * i + R * N * k];
-          }
-          s[k] = mac<F>(mac<F>(mac<F>(s[k], a0, r0), b0, s0),
-                        c_dslab[N][l + N * k], wt[l]);
-          if (l + 1 < N)
-            s[k] = mac<F>(mac<F>(mac<F>(s[k], a1, r1), b1, s1),
-                          c_dslab[N][l + 1 + N * k], wt[l + 1]);
-        }
-      }
-      double *we = w + e * NP + i + N * j;
-#pragma unroll
-      for (int k = 0; k < N; ++k) {
-        we[N2 * k] = s[k];
-        if constexpr (SUMSQ) acc = dadd(acc, dmul(s[k], s[k]));
-      }
-    }
-    named_bar_sync(1 + grp, T);
-  }
-
-  if constexpr (SUMSQ) block_sumsq_partial(acc, partials);
-}
-
-template <int N, int G, int SGS, int KS, bool DREG, bool F, bool V2 = false>
+template <int N, int G, int SGS, int KS, bool DREG, bool F>
 int launch_sem_slab(double *w, const double *u, const double *d,
                     const double *g, int64_t nelt, const lfb_launch *geom,
                     cudaStream_t s, int64_t *grid_out) {
@@ -521,15 +293,8 @@ int launch_sem_slab(double *w, const double *u, const double *d,
   const bool sumsq = geom && geom->sumsq;
   if (sumsq && (!geom->workspace || geom->workspace_len < grid))
     return fail(LFB_ERR_ARG, "semlap: sumsq workspace too small");
-  auto pick = [&]() {
-    if constexpr (V2)
-      return sumsq ? semlap_slab2_kernel<N, G, SGS, KS, DREG, true, F>
-                   : semlap_slab2_kernel<N, G, SGS, KS, DREG, false, F>;
-    else
-      return sumsq ? semlap_slab_kernel<N, G, SGS, KS, DREG, true, F>
-                   : semlap_slab_kernel<N, G, SGS, KS, DREG, false, F>;
-  };
-  auto k = pick();
+  auto k = sumsq ? semlap_slab_kernel<N, G, SGS, KS, DREG, true, F>
+                 : semlap_slab_kernel<N, G, SGS, KS, DREG, false, F>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)L::total);
   {
@@ -575,31 +340,10 @@ int launch_sem_slab(double *w, const double *u, const double *d,
   X(16, 30, 1, 3, 1, false)     \
   X(16, 31, 1, 3, 2, false)
 
-// variants 32 (bitwise) / 33 (DFMA): the l-outer kernel (semlap_slab2),
-// (groups, ring depth, slices per copy, d in registers) per n
-#define LFB_SLAB2_TABLE(X)  \
-  X(9, 3, 4, 3, true)       \
-  X(10, 3, 4, 2, true)      \
-  X(11, 3, 4, 1, true)      \
-  X(12, 2, 3, 2, true)      \
-  X(13, 2, 4, 1, true)      \
-  X(14, 1, 4, 2, true)      \
-  X(15, 1, 3, 2, false)     \
-  X(16, 1, 2, 3, false)
-
 int sem_slab_dispatch(int n, int variant, double *w, const double *u,
                       const double *d, const double *g, int64_t nelt,
                       const lfb_launch *geom, cudaStream_t s,
                       int64_t *grid_out) {
-#define X(NN, GG, SS, KK, DR)                                               \
-  if (n == NN && (variant == 32 || variant == 33))                          \
-    return variant == 32                                                    \
-               ? launch_sem_slab<NN, GG, SS, KK, DR, false, true>(          \
-                     w, u, d, g, nelt, geom, s, grid_out)                   \
-               : launch_sem_slab<NN, GG, SS, KK, DR, true, true>(           \
-                     w, u, d, g, nelt, geom, s, grid_out);
-  LFB_SLAB2_TABLE(X)
-#undef X
   const int v = variant == 9 ? 0 : variant;
 #define X(NN, VV, GG, SS, KK, DR)                                         \
   if (n == NN && v == VV)                                                 \
