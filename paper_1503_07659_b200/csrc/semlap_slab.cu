@@ -440,27 +440,16 @@ __global__ void __launch_bounds__(G *HCfg<N>::T, 1)
               const double *col = su + i + N2 * k;
 #pragma unroll
               for (int l = 0; l < N; l += 2) {
-                // d(i, l..l+1) and d(j, l..l+1) as 16-byte pairs of the
-                // transposed copy (dt[b + N a] = d(a, b)): half the loads
-                double r0, r1 = 0.0, a0, a1 = 0.0, b0, b1 = 0.0;
-                if (l + 1 < N) {
-                  slab_pair<N>(row + l, r0, r1);
-                  if constexpr (DREG) {
-                    a0 = da[l], a1 = da[l + 1], b0 = db[l], b1 = db[l + 1];
-                  } else {
-                    slab_pair<N>(dt + l + N * i, a0, a1);
-                    slab_pair<N>(dt + l + N * j, b0, b1);
-                  }
-                } else {
-                  r0 = row[l];
-                  a0 = DREG ? da[l] : dt[l + N * i];
-                  b0 = DREG ? db[l] : dt[l + N * j];
-                }
+                double r0, r1 = 0.0;
+                if (l + 1 < N) slab_pair<N>(row + l, r0, r1);
+                else r0 = row[l];
 #pragma unroll
                 for (int t = 0; t < 2 && l + t < N; ++t) {
                   const int ll = l + t;
-                  ur = mac<F>(ur, t ? a1 : a0, t ? r1 : r0);
-                  us = mac<F>(us, t ? b1 : b0, col[N * ll]);
+                  const double a = DREG ? da[ll] : dn[i + N * ll];
+                  const double b = DREG ? db[ll] : dn[j + N * ll];
+                  ur = mac<F>(ur, a, t ? r1 : r0);
+                  us = mac<F>(us, b, col[N * ll]);
                   ut = mac<F>(ut, c_dslab[N][k + N * ll], ucol[ll]);
                 }
               }
@@ -471,8 +460,7 @@ __global__ void __launch_bounds__(G *HCfg<N>::T, 1)
               const double2 g45 = *reinterpret_cast<const double2 *>(gp + 4);
               scr_r[i + R * j + R * N * k] =
                   comb3<F>(g01.x, ur, g01.y, us, g23.x, ut);
-              // ws stored transposed: ws(i, l, k) at scr_s[l + R i + R N k]
-              scr_s[j + R * i + R * N * k] =
+              scr_s[i + R * j + R * N * k] =
                   comb3<F>(g01.y, ur, g23.y, us, g45.x, ut);
               wts[i + N * j + N2 * k] =
                   comb3<F>(g23.x, ur, g45.x, us, g45.y, ut);
@@ -511,32 +499,19 @@ __global__ void __launch_bounds__(G *HCfg<N>::T, 1)
           const int k = kk + hh;
           if (hh == h && k < N) {
             double s = 0.0;
-            const double *rr = scr_r + R * j + R * N * k;  // wr(., j, k)
-            const double *rs = scr_s + R * i + R * N * k;  // ws(i, ., k)
+            const double *rr = scr_r + R * j + R * N * k;
+            const double *rs = scr_s + i + R * N * k;
 #pragma unroll
             for (int l = 0; l < N; l += 2) {
-              // d(l..l+1, i), d(l..l+1, j): 16-byte pairs of d itself
-              double r0, r1 = 0.0, s0, s1 = 0.0, a0, a1 = 0.0, b0, b1 = 0.0;
-              if (l + 1 < N) {
-                slab_pair<N>(rr + l, r0, r1);
-                slab_pair<N>(rs + l, s0, s1);
-                if constexpr (DREG) {
-                  a0 = da[l], a1 = da[l + 1], b0 = db[l], b1 = db[l + 1];
-                } else {
-                  slab_pair<N>(dn + l + N * i, a0, a1);
-                  slab_pair<N>(dn + l + N * j, b0, b1);
-                }
-              } else {
-                r0 = rr[l];
-                s0 = rs[l];
-                a0 = DREG ? da[l] : dn[l + N * i];
-                b0 = DREG ? db[l] : dn[l + N * j];
-              }
+              double r0, r1 = 0.0;
+              if (l + 1 < N) slab_pair<N>(rr + l, r0, r1);
+              else r0 = rr[l];
 #pragma unroll
               for (int t = 0; t < 2 && l + t < N; ++t) {
                 const int ll = l + t;
-                s = mac<F>(mac<F>(mac<F>(s, t ? a1 : a0, t ? r1 : r0),
-                                  t ? b1 : b0, t ? s1 : s0),
+                const double a = DREG ? da[ll] : dt[i + N * ll];
+                const double b = DREG ? db[ll] : dt[j + N * ll];
+                s = mac<F>(mac<F>(mac<F>(s, a, t ? r1 : r0), b, rs[R * ll]),
                            c_dslab[N][ll + N * k], wtc[ll]);
               }
             }
@@ -595,9 +570,9 @@ int launch_sem_slabh(double *w, const double *u, const double *d,
 // (n) -> (groups, slab-pair ring depth, d rows in registers)
 #define LFB_SLABH_TABLE(X) \
   X(9, 2, 3, true)         \
-  X(10, 2, 2, false)       \
+  X(10, 2, 3, true)        \
   X(11, 1, 4, true)        \
-  X(12, 2, 2, false)       \
+  X(12, 1, 4, true)        \
   X(13, 1, 4, false)       \
   X(14, 1, 3, false)       \
   X(15, 1, 2, false)       \
