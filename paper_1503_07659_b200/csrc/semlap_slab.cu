@@ -272,314 +272,6 @@ __global__ void __launch_bounds__(G *SlabCfg<N>::T, 1)
   if constexpr (SUMSQ) block_sumsq_partial(acc, partials);
 }
 
-// {{{ two threads per k-column (variants 35 bitwise / 36 DFMA)
-//
-// The slab kernel above gives thread (i, j) the whole k-column: its u column
-// and wt column live in registers (>= 2n doubles) and at n >= 13 only one or
-// two n^2-thread groups fit per SM -- 8-12 warps, FP64 pipe ~50 % busy,
-// latency bound (ncu, profiles/r01_sem_hi_16_0.md).  Here the column is
-// shared by two threads, h = 0 / 1 taking the slices k = h, h + 2, ... in
-// both phases: wt goes to shared memory (it is read across halves in
-// phase 2), u has a single stage (the next element's u lands during phase
-// 2, which does not read it), the g ring holds pairs of slices (one bulk
-// copy per step, slice 2s for h = 0, 2s + 1 for h = 1).  Twice the warps per
-// element at about half the registers per thread.  Same arithmetic, same
-// association: every chain is one thread's, l ascending.
-template <int N>
-struct HCfg {
-  static constexpr int N2 = N * N;
-  static constexpr int NP = N * N * N;
-  static constexpr int T = ((2 * N2 + 31) / 32) * 32;
-  static constexpr int R = (N % 2 == 0) ? N + 2 : N + 1;
-  static constexpr int SCR = R * N * N;
-  static constexpr int UST = (NP + 2 + 1) / 2 * 2;
-  static constexpr int SLAB = 6 * N2;
-  static constexpr int STEPS = (N + 1) / 2;
-};
-
-template <int N, int G, int SGS>
-struct HSmem {
-  using C = HCfg<N>;
-  static constexpr size_t bars = 256;
-  static constexpr size_t d_off = bars;
-  static constexpr size_t grp_off = (d_off + 2 * N * N * 8 + 127) / 128 * 128;
-  static constexpr size_t grp_bytes =
-      (((size_t)C::UST + (size_t)SGS * 2 * C::SLAB + 2 * (size_t)C::SCR +
-        (size_t)C::NP) * 8 + 127) / 128 * 128;
-  static constexpr size_t total = grp_off + G * grp_bytes;
-};
-
-template <int N, int G, int SGS, bool DREG, bool SUMSQ, bool F>
-__global__ void __launch_bounds__(G *HCfg<N>::T, 1)
-    semlap_slabh_kernel(double *__restrict__ w, const double *__restrict__ u,
-                        const double *__restrict__ d,
-                        const double *__restrict__ g, int64_t nelt,
-                        double *__restrict__ partials) {
-  using C = HCfg<N>;
-  using L = HSmem<N, G, SGS>;
-  constexpr int NP = C::NP, N2 = C::N2, T = C::T, R = C::R;
-  constexpr int STEPS = C::STEPS;
-  static_assert(G * (1 + SGS) <= 32, "too many mbarriers");
-
-  extern __shared__ __align__(128) unsigned char smem[];
-  uint64_t *bars = reinterpret_cast<uint64_t *>(smem);
-  double *dn = reinterpret_cast<double *>(smem + L::d_off);
-  double *dt = dn + N2;
-
-  const int tid = threadIdx.x;
-  const int grp = tid / T;
-  const int lt = tid % T;
-  const int h = lt / N2;          // which slices: k = h, h + 2, ...
-  const int c = lt % N2;
-  const int i = c % N;
-  const int j = c / N;
-  const bool active = lt < 2 * N2;
-
-  unsigned char *gbase = smem + L::grp_off + (size_t)grp * L::grp_bytes;
-  double *ust = reinterpret_cast<double *>(gbase);        // UST
-  double *slabs = ust + C::UST;                           // SGS x 2 x SLAB
-  double *scr_r = slabs + SGS * 2 * C::SLAB;              // SCR
-  double *scr_s = scr_r + C::SCR;                         // SCR
-  double *wts = scr_s + C::SCR;                           // NP: wt(i,j,k)
-  uint64_t *ubar = bars + grp * (1 + SGS);
-  uint64_t *gbar = ubar + 1;
-
-  const int64_t q0 = (int64_t)blockIdx.x * G + grp;
-  const int64_t Q = (int64_t)gridDim.x * G;
-  const int64_t mine = nelt > q0 ? (nelt - q0 + Q - 1) / Q : 0;
-  auto elem = [&](int64_t m) -> int64_t { return q0 + m * Q; };
-
-  if (tid == 0) {
-    for (int q = 0; q < G * (1 + SGS); ++q) mbar_init(&bars[q], 1);
-    fence_mbar_init();
-  }
-  __syncthreads();
-
-  const uint64_t pol = policy_evict_first();
-  const int64_t u_bytes_total = nelt * NP * 8;
-  auto u_lead = [&](int64_t e) -> int { return (int)((e * NP) & 1); };
-  auto u_span = [&](int64_t e) -> int64_t {
-    return ((int64_t)(u_lead(e) + NP) * 8 + 15) / 16 * 16;
-  };
-  auto u_bulk_ok = [&](int64_t e) -> bool {
-    return (e * NP - u_lead(e)) * 8 + u_span(e) <= u_bytes_total;
-  };
-  auto issue_u = [&](int64_t m) {
-    const int64_t e = elem(m);
-    if (u_bulk_ok(e)) {
-      mbar_arrive_expect_tx(ubar, (uint32_t)u_span(e));
-      bulk_g2s_stream(ust, u + e * NP - u_lead(e), (uint32_t)u_span(e), ubar,
-                      pol);
-    } else {
-      mbar_arrive_expect_tx(ubar, 0);  // threads copy it themselves
-    }
-  };
-  auto issue_slab = [&](int64_t q) {  // q = m * STEPS + step
-    const int64_t m = q / STEPS;
-    const int step = (int)(q % STEPS);
-    const int k0 = 2 * step;
-    const int nk = (N - k0) < 2 ? (N - k0) : 2;
-    const int64_t e = elem(m);
-    const int slot = (int)(q % SGS);
-    mbar_arrive_expect_tx(&gbar[slot], (uint32_t)(nk * C::SLAB * 8));
-    bulk_g2s_stream(slabs + (size_t)slot * 2 * C::SLAB,
-                    g + e * 6 * NP + (int64_t)k0 * 6 * N2, nk * C::SLAB * 8,
-                    &gbar[slot], pol);
-  };
-
-  const int64_t nsteps = mine * STEPS;
-  if (lt == 0) {
-    if (mine > 0) issue_u(0);
-    for (int64_t q = 0; q < SGS && q < nsteps; ++q) issue_slab(q);
-  }
-  for (int q = tid; q < N2; q += G * T) {
-    const double v = d[q];
-    dn[q] = v;
-    dt[(q / N) + N * (q % N)] = v;
-  }
-  __syncthreads();
-
-  double acc = 0.0;
-  for (int64_t m = 0; m < mine; ++m) {
-    const int64_t e = elem(m);
-    mbar_wait(ubar, (uint32_t)(m & 1));
-    const double *su = ust + u_lead(e);
-    if (!u_bulk_ok(e)) {
-      for (int q = lt; q < NP; q += T) ust[u_lead(e) + q] = u[e * NP + q];
-      named_bar_sync(1 + grp, T);
-    }
-
-    // ---- phase 1: slices k = 2 step + h
-    {
-      double ucol[N];
-      double da[N], db[N];
-      if (active) {
-#pragma unroll
-        for (int l = 0; l < N; ++l) ucol[l] = su[i + N * j + N2 * l];
-        if constexpr (DREG) {
-#pragma unroll
-          for (int l = 0; l < N; ++l)
-            da[l] = dn[i + N * l], db[l] = dn[j + N * l];
-        }
-      }
-#pragma unroll
-      for (int step = 0; step < STEPS; ++step) {
-        const int64_t q = m * STEPS + step;
-        const int slot = (int)(q % SGS);
-        mbar_wait(&gbar[slot], (uint32_t)((q / SGS) & 1));
-        const int k0 = 2 * step;
-        if (active && k0 + h < N) {
-          // the two halves take the two slices of the step; the k-dependent
-          // constant-bank operand d(k,l) needs a static k, so branch on h
-#pragma unroll
-          for (int hh = 0; hh < 2; ++hh) {
-            const int k = k0 + hh;
-            if (hh == h && k < N) {
-              double ur = 0.0, us = 0.0, ut = 0.0;
-              const double *row = su + N * j + N2 * k;
-              const double *col = su + i + N2 * k;
-#pragma unroll
-              for (int l = 0; l < N; l += 2) {
-                double r0, r1 = 0.0;
-                if (l + 1 < N) slab_pair<N>(row + l, r0, r1);
-                else r0 = row[l];
-#pragma unroll
-                for (int t = 0; t < 2 && l + t < N; ++t) {
-                  const int ll = l + t;
-                  const double a = DREG ? da[ll] : dn[i + N * ll];
-                  const double b = DREG ? db[ll] : dn[j + N * ll];
-                  ur = mac<F>(ur, a, t ? r1 : r0);
-                  us = mac<F>(us, b, col[N * ll]);
-                  ut = mac<F>(ut, c_dslab[N][k + N * ll], ucol[ll]);
-                }
-              }
-              const double *gp = slabs + (size_t)slot * 2 * C::SLAB +
-                                 hh * C::SLAB + 6 * (i + N * j);
-              const double2 g01 = *reinterpret_cast<const double2 *>(gp);
-              const double2 g23 = *reinterpret_cast<const double2 *>(gp + 2);
-              const double2 g45 = *reinterpret_cast<const double2 *>(gp + 4);
-              scr_r[i + R * j + R * N * k] =
-                  comb3<F>(g01.x, ur, g01.y, us, g23.x, ut);
-              scr_s[i + R * j + R * N * k] =
-                  comb3<F>(g01.y, ur, g23.y, us, g45.x, ut);
-              wts[i + N * j + N2 * k] =
-                  comb3<F>(g23.x, ur, g45.x, us, g45.y, ut);
-            }
-          }
-        }
-        named_bar_sync(1 + grp, T);  // slot consumed (last step: u too)
-        if (lt == 0) {
-          if (q + SGS < nsteps) {
-            fence_proxy_async_smem();
-            issue_slab(q + SGS);
-          }
-          if (step == STEPS - 1 && m + 1 < mine) {
-            fence_proxy_async_smem();
-            issue_u(m + 1);  // lands during phase 2, which reads no u
-          }
-        }
-      }
-    }
-
-    // ---- phase 2: outputs k = h, h + 2, ...
-    if (active) {
-      double wtc[N];
-      double da[N], db[N];
-#pragma unroll
-      for (int l = 0; l < N; ++l) wtc[l] = wts[i + N * j + N2 * l];
-      if constexpr (DREG) {
-#pragma unroll
-        for (int l = 0; l < N; ++l) da[l] = dt[i + N * l], db[l] = dt[j + N * l];
-      }
-      double *we = w + e * NP + i + N * j;
-#pragma unroll
-      for (int kk = 0; kk < N; kk += 2) {
-#pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
-          const int k = kk + hh;
-          if (hh == h && k < N) {
-            double s = 0.0;
-            const double *rr = scr_r + R * j + R * N * k;
-            const double *rs = scr_s + i + R * N * k;
-#pragma unroll
-            for (int l = 0; l < N; l += 2) {
-              double r0, r1 = 0.0;
-              if (l + 1 < N) slab_pair<N>(rr + l, r0, r1);
-              else r0 = rr[l];
-#pragma unroll
-              for (int t = 0; t < 2 && l + t < N; ++t) {
-                const int ll = l + t;
-                const double a = DREG ? da[ll] : dt[i + N * ll];
-                const double b = DREG ? db[ll] : dt[j + N * ll];
-                s = mac<F>(mac<F>(mac<F>(s, a, t ? r1 : r0), b, rs[R * ll]),
-                           c_dslab[N][ll + N * k], wtc[ll]);
-              }
-            }
-            we[N2 * k] = s;
-            if constexpr (SUMSQ) acc = dadd(acc, dmul(s, s));
-          }
-        }
-      }
-    }
-    named_bar_sync(1 + grp, T);  // scratch reads done before next phase 1
-  }
-
-  if constexpr (SUMSQ) block_sumsq_partial(acc, partials);
-}
-
-template <int N, int G, int SGS, bool DREG, bool F>
-int launch_sem_slabh(double *w, const double *u, const double *d,
-                     const double *g, int64_t nelt, const lfb_launch *geom,
-                     cudaStream_t s, int64_t *grid_out) {
-  using L = HSmem<N, G, SGS>;
-  static_assert(L::total <= 227 * 1024, "smem");
-  const int block = G * HCfg<N>::T;
-  int sms = sm_count(geom);
-  if (sms <= 0) sms = 148;
-  int64_t grid64 = sms;
-  if (grid64 * G > nelt) grid64 = (nelt + G - 1) / G;
-  if (grid64 < 1) grid64 = 1;
-  const int grid = (int)grid64;
-  if (grid_out) {
-    *grid_out = grid;
-    return LFB_OK;
-  }
-  const bool sumsq = geom && geom->sumsq;
-  if (sumsq && (!geom->workspace || geom->workspace_len < grid))
-    return fail(LFB_ERR_ARG, "semlap: sumsq workspace too small");
-  auto k = sumsq ? semlap_slabh_kernel<N, G, SGS, DREG, true, F>
-                 : semlap_slabh_kernel<N, G, SGS, DREG, false, F>;
-  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)L::total);
-  {
-    std::unique_lock<std::mutex> lk;
-    bool capturing = false;
-    int slot = N;
-    if (int rc = dconst_acquire(c_dslab, 256 * 8, 2, &slot, d, N, s, &lk,
-                                &capturing))
-      return rc;
-    k<<<grid, block, L::total, s>>>(w, u, d, g, nelt,
-                                    sumsq ? geom->workspace : nullptr);
-    dconst_release(2, slot, s, capturing);
-  }
-  if (int rc = check_launch("lfb_semlap_f64")) return rc;
-  return sumsq ? sem_sumsq_finish(geom->workspace, grid, geom->sumsq, s)
-               : LFB_OK;
-}
-
-// (n) -> (groups, slab-pair ring depth, d rows in registers)
-#define LFB_SLABH_TABLE(X) \
-  X(9, 2, 3, true)         \
-  X(10, 2, 3, true)        \
-  X(11, 1, 4, true)        \
-  X(12, 1, 4, true)        \
-  X(13, 1, 4, false)       \
-  X(14, 1, 3, false)       \
-  X(15, 1, 2, false)       \
-  X(16, 1, 2, false)
-
-// }}}
-
 template <int N, int G, int SGS, int KS, bool DREG, bool F>
 int launch_sem_slab(double *w, const double *u, const double *d,
                     const double *g, int64_t nelt, const lfb_launch *geom,
@@ -653,15 +345,6 @@ int sem_slab_dispatch(int n, int variant, double *w, const double *u,
                       const double *d, const double *g, int64_t nelt,
                       const lfb_launch *geom, cudaStream_t s,
                       int64_t *grid_out) {
-#define X(NN, GG, SS, DR)                                                   \
-  if (n == NN && (variant == 35 || variant == 36))                          \
-    return variant == 35                                                    \
-               ? launch_sem_slabh<NN, GG, SS, DR, false>(w, u, d, g, nelt,  \
-                                                         geom, s, grid_out) \
-               : launch_sem_slabh<NN, GG, SS, DR, true>(w, u, d, g, nelt,   \
-                                                        geom, s, grid_out);
-  LFB_SLABH_TABLE(X)
-#undef X
   const int v = variant == 9 ? 0 : variant;
 #define X(NN, VV, GG, SS, KK, DR)                                         \
   if (n == NN && v == VV)                                                 \
