@@ -615,7 +615,7 @@ static int sem_dispatch(double *w, const double *u, const double *d,
                                      nelt, geom, s, grid_out);
     if (rc != -1) return rc;
   }
-  if (((var0 >= 51 && var0 <= 54) || var0 == 56 || var0 == 57) ||
+  if ((var0 >= 51 && var0 <= 54) ||
       (var0 == 50 && (n == 7 || n == 8 || n >= 12))) {
     // FP64 tensor cores (semlap_tc.cu), n = 8..16; the interleaved-phase
     // kernel (52) is the DFMA-mode default for n >= 12, where it beats the

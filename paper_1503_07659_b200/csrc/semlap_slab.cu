@@ -338,8 +338,7 @@ int launch_sem_slab(double *w, const double *u, const double *d,
   X(15, 30, 1, 4, 1, false)     \
   X(16, 0, 1, 2, 3, false)      \
   X(16, 30, 1, 3, 1, false)     \
-  X(16, 31, 1, 3, 2, false)     \
-  X(12, 34, 3, 2, 1, false)
+  X(16, 31, 1, 3, 2, false)
 
 int sem_slab_dispatch(int n, int variant, double *w, const double *u,
                       const double *d, const double *g, int64_t nelt,

@@ -781,13 +781,7 @@ static int launch_tc(double *w, const double *u, const double *d,
   X(13, 53, 2, 3, 1)     \
   X(14, 53, 2, 3, 1)     \
   X(15, 53, 2, 3, 1)     \
-  X(16, 53, 2, 3, 1)     \
-  X(12, 56, 4, 2, 2)     \
-  X(13, 56, 4, 2, 1)     \
-  X(14, 56, 4, 2, 1)     \
-  X(15, 56, 4, 2, 1)     \
-  X(16, 56, 3, 2, 1)     \
-  X(16, 57, 3, 2, 2)
+  X(16, 53, 2, 3, 1)
 
 int sem_tc_dispatch(int n, int variant, double *w, const double *u,
                     const double *d, const double *g, int64_t nelt,
