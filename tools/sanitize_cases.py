@@ -121,6 +121,37 @@ def generic_prefetch():
     return ok
 
 
+def assembly():
+    """dssum (every mode through the 2-slab protocol) and a traced run."""
+    from paper_1503_07659_b200.assembly import BoxMesh, _launch, dssum
+    mesh = BoxMesh(3, 2, 4, 5)
+    w = torch.rand(mesh.nelt * 125, dtype=torch.float64, device=dev)
+    ref = oracle.dssum(w.cpu().numpy(), 5, 3, 2, 4)
+    whole = w.clone()
+    dssum(whole, mesh)
+    per = 3 * 2 * 125
+    lo, hi = w[:2 * per], w[2 * per:]
+    s_lo, s_hi = mesh.slab(0, 2), mesh.slab(1, 2)
+    _launch(lo, s_lo, 0, s_lo.top - 1, 0)
+    _launch(hi, s_hi, 1, s_hi.top, 0)
+    part = torch.empty(mesh.plane, dtype=torch.float64, device=dev)
+    tot = torch.empty_like(part)
+    _launch(lo, s_lo, s_lo.top, s_lo.top, 1, None, part)
+    _launch(hi, s_hi, 0, 0, 2, part, tot)
+    _launch(lo, s_lo, s_lo.top, s_lo.top, 3, tot, None)
+    torch.cuda.synchronize()
+    ok = whole.cpu().numpy().tobytes() == ref.tobytes() and \
+        torch.equal(w, whole)
+    _r, kg = fx.translate(fx.gemm_source("f64"))
+    env = lfb.make_device_env(kg, {"m": 20, "n": 12, "l": 40},
+                              {"alpha": 0.5}, seed=3, trace=True, device=dev)
+    out = lfb.interpret(kg, env)
+    ok &= len(out.write_trace) > 0
+    print(f"dssum modes / write trace: {'ok' if ok else 'MISMATCH'}",
+          flush=True)
+    return ok
+
+
 if __name__ == "__main__":
     which = sys.argv[1] if len(sys.argv) > 1 else "all"
     oks = []
@@ -136,6 +167,8 @@ if __name__ == "__main__":
                 gemm("f64", 100, 60, 33, 1, True)]
     if which in ("all", "stream"):
         oks.append(streams())
+    if which in ("all", "assembly"):
+        oks.append(assembly())
     if which in ("all", "generic"):
         oks += [generic_gemm(64, 40, 96, True), generic_gemm(37, 20, 45, False),
                 generic_prefetch()]
