@@ -584,6 +584,63 @@ def cpu_reference(n, sample_elems, threads, min_seconds):
                       + f" on {threads} thread(s)",
             "seconds": dt * reps}
 
+def cpu_reference_full(n, nelt, threads, steps, warmup):
+    """The reference arm on the full config: every step runs the reference's
+    emitted C (oracle/_ref, cc -std=c99 -O1) over all *nelt* elements on
+    *threads* host threads (element chunks of <= 699,050, multiples of 32:
+    its int indexing and its assume(nelt mod 32 = 0)).  Inputs: a 65,536-
+    element random sample tiled over the full arrays (64 GiB at 2^21
+    elements of order 7) -- the same work per element.  Returns the per-step
+    times (s) or None when the host cannot hold the arrays."""
+    import concurrent.futures as cf
+    import ctypes as C
+
+    import numpy as np
+    sys.path.insert(0, os.path.join(REPO, "oracle"))
+    import oracle
+    if not oracle.have_ref():
+        return None
+    np3 = n ** 3
+    need = 64 * np3 * nelt
+    try:
+        import psutil
+        if psutil.virtual_memory().available < need * 1.4:
+            return None
+    except Exception:
+        return None
+    sample = min(65536, nelt)
+    rng = np.random.default_rng(0)
+    su = rng.random(sample * np3) * 2 - 1
+    sg = rng.random(6 * sample * np3)
+    d = rng.random(n * n) * 2 - 1
+    u = np.empty(nelt * np3)
+    g = np.empty(6 * nelt * np3)
+    w = np.zeros(nelt * np3)
+    for e0 in range(0, nelt, sample):
+        m = min(sample, nelt - e0)
+        u[e0 * np3:(e0 + m) * np3] = su[:m * np3]
+        g[6 * e0 * np3:6 * (e0 + m) * np3] = sg[:6 * m * np3]
+    P, I = C.c_void_p, C.c_int
+    fn = oracle.ref_fn(f"ref_semlap_n{n}", [P, P, P, P, I])
+    per = min(699040, max(32, nelt // threads // 32 * 32))
+    cuts = list(range(0, nelt, per)) + [nelt]
+    ranges = [(cuts[c], cuts[c + 1]) for c in range(len(cuts) - 1)]
+
+    def run(r):
+        e0, e1 = r
+        fn(C.c_void_p(w.ctypes.data + e0 * np3 * 8),
+           C.c_void_p(u.ctypes.data + e0 * np3 * 8), d.ctypes.data_as(P),
+           C.c_void_p(g.ctypes.data + 6 * e0 * np3 * 8), e1 - e0)
+
+    times = []
+    with cf.ThreadPoolExecutor(threads) as pool:
+        for _ in range(warmup + steps):
+            t0 = time.perf_counter()
+            list(pool.map(run, ranges))
+            times.append(time.perf_counter() - t0)
+    return times[warmup:]
+
+
 def _host_threads():
     try:
         return len(os.sched_getaffinity(0))
@@ -1400,14 +1457,30 @@ def main():
         # the reference's own CPU execution of the path, rank 0 only
         if int(os.environ.get("RANK", "0")) != 0:
             return
-        sample = 65536
-        per_step = []
-        cpu = None
-        for _ in range(args.warmup + args.steps):
-            cpu = cpu_reference(args.npts, sample, threads, 1.0)
-            per_step.append(cpu["value"])
-        value = statistics.median(per_step[args.warmup:])
-        cpu["value"] = value
+        np3 = args.npts ** 3
+        full = None if args.workload != "sem2m" else cpu_reference_full(
+            args.npts, args.nelt, threads, args.steps, args.warmup)
+        if full is not None:
+            step_s = statistics.median(full)
+            value = args.nelt * np3 / step_s / 1e9
+            sample = args.nelt
+            cpu = {"value": value, "unit": "GDOF/s", "cores": threads,
+                   "kind": "reference",
+                   "sample": f"the full config: all {args.nelt} elements "
+                             f"(n={args.npts}) every step, {args.steps} "
+                             f"timed steps after {args.warmup}; the "
+                             "reference's emitted C (codegen.emit, cc "
+                             f"-std=c99 -O1) on {threads} thread(s)",
+                   "step_seconds": full}
+        else:
+            sample = 65536
+            per_step = []
+            cpu = None
+            for _ in range(args.warmup + args.steps):
+                cpu = cpu_reference(args.npts, sample, threads, 1.0)
+                per_step.append(cpu["value"])
+            value = statistics.median(per_step[args.warmup:])
+            cpu["value"] = value
         res = {"metric": METRIC, "value": value, "unit": "GDOF/s",
                "impl": "reference", "n_gpus": args.gpus,
                "steps": args.steps, "warmup": args.warmup,
@@ -1417,9 +1490,12 @@ def main():
                "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                "config": {"workload": f"semlap order {args.npts - 1} "
                                       f"(n={args.npts}) fp64, {args.nelt} "
-                                      "elements; each step times a "
-                                      f"{sample}-element sample",
-                          "nelt": args.nelt, "npts": args.npts},
+                                      "elements; each step times "
+                                      + ("all of them" if sample ==
+                                         args.nelt else
+                                         f"a {sample}-element sample"),
+                          "nelt": args.nelt, "npts": args.npts,
+                          "same_config": sample == args.nelt},
                "cpu_baseline": cpu,
                "e2e": {"value": value, "unit": "GDOF/s",
                        "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
