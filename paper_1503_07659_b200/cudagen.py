@@ -275,7 +275,11 @@ class Program:
 
 
 class _Emitter:
-    def __init__(self, kernel, checked=None, trace=False):
+    # per-work-item (local memory) / per-work-group (shared memory) bytes of
+    # one temporary
+    TEMP_BYTES_MAX = 48 * 1024
+
+    def __init__(self, kernel, checked=None, trace=False, params=None):
         k = transforms.expand_all_rules(kernel) if kernel.rules else kernel
         lfk.validate_kernel(k)
         self.k = k
@@ -327,11 +331,30 @@ class _Emitter:
             if t.shape:
                 shape = []
                 for s in t.shape:
-                    if not s.is_constant():
+                    if s.is_constant():
+                        shape.append(s.constant)
+                    elif params is not None and s.variables <= set(params):
+                        # extent from the launch's parameters, as the
+                        # reference allocates it (interp.py:332-338): the
+                        # program is specialised to those values
+                        shape.append(int(s.eval(params)))
+                    else:
                         raise CodegenError(
                             f"temporary '{t.name}' has a symbolic extent; "
-                            "the CUDA emitter needs constant extents")
-                    shape.append(s.constant)
+                            "the CUDA emitter needs constant extents (or "
+                            "the parameter values)")
+                if any(x <= 0 for x in shape):
+                    raise CodegenError(
+                        f"temporary '{t.name}' has non-positive extent "
+                        f"{tuple(shape)}")
+                size = 8
+                for x in shape:
+                    size *= x
+                if size > self.TEMP_BYTES_MAX:
+                    raise CodegenError(
+                        f"temporary '{t.name}' of {size} bytes exceeds the "
+                        f"{self.TEMP_BYTES_MAX}-byte per-work-item / "
+                        "work-group budget of the CUDA emitter")
                 self.temp_shapes[t.name] = tuple(shape)
                 alloc = list(shape)
                 if t.address_space == "workgroup" and len(shape) >= 2 \
@@ -1709,12 +1732,25 @@ class _Emitter:
                              for q in range(len(self.insn_ids))))
 
 
-def emit_cuda(kernel, checked=None, trace=False):
+def emit_cuda(kernel, checked=None, trace=False, params=None):
     """Render *kernel* (transformed, rules expanded or not) as one CUDA
     kernel; returns a :class:`Program`.  *checked*: None, "plain" (the
     reference's interpret() checks) or "dims" (interpret_bounds_checked).
-    *trace*: also record every store (make_env(trace=True))."""
-    return _Emitter(kernel, checked, trace).emit()
+    *trace*: also record every store (make_env(trace=True)).  *params*:
+    parameter values for temporaries whose extents depend on them (the
+    program is then specialised to those values)."""
+    return _Emitter(kernel, checked, trace, params).emit()
 
 
-__all__ = ["Program", "TmaMap", "emit_cuda", "NVRTC_OPTIONS", "promote"]
+def temp_params(kernel):
+    """Parameters the temporaries' extents depend on (sorted)."""
+    k = transforms.expand_all_rules(kernel) if kernel.rules else kernel
+    names = set()
+    for t in k.temporaries.values():
+        for s in t.shape:
+            names |= set(s.variables)
+    return tuple(sorted(names))
+
+
+__all__ = ["Program", "TmaMap", "emit_cuda", "temp_params", "NVRTC_OPTIONS",
+           "promote"]

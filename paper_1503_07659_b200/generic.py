@@ -15,7 +15,7 @@ import torch
 
 from . import abi
 from ._loopforge import InterpError
-from .cudagen import NVRTC_OPTIONS, emit_cuda
+from .cudagen import NVRTC_OPTIONS, emit_cuda, temp_params
 from .launch import launch_geometry
 
 _CUBINS = {}    # program key -> cubin bytes
@@ -23,14 +23,22 @@ _MODULES = {}   # (program key, device index) -> lfb_module handle
 _PROGRAMS = {}  # id(kernel) -> (kernel, Program)
 
 
-def program_for(kernel, checked=None, trace=False):
-    hit = _PROGRAMS.get((id(kernel), checked, trace))
+def program_for(kernel, checked=None, trace=False, params=None):
+    """The generated program of *kernel* (cached per kernel and build
+    flavour).  Temporaries whose extents depend on parameters specialise
+    the program to those parameters' values (*params*), as the reference
+    sizes them per call (interp.py:332-338)."""
+    tp = temp_params(kernel)
+    spec = tuple((p, int(params[p])) for p in tp) if tp and params else ()
+    key = (id(kernel), checked, trace, spec)
+    hit = _PROGRAMS.get(key)
     if hit is not None and hit[0] is kernel:
         return hit[1]
-    prog = emit_cuda(kernel, checked=checked, trace=trace)
+    prog = emit_cuda(kernel, checked=checked, trace=trace,
+                     params=dict(spec) if spec else None)
     if len(_PROGRAMS) > 256:
         _PROGRAMS.clear()
-    _PROGRAMS[(id(kernel), checked, trace)] = (kernel, prog)
+    _PROGRAMS[key] = (kernel, prog)
     return prog
 
 
@@ -143,7 +151,7 @@ class GenericLauncher:
     def __init__(self, kernel, env, checked=None, trace=False):
         self.kernel = kernel
         self.env = env
-        self.program = program_for(kernel, checked, trace)
+        self.program = program_for(kernel, checked, trace, env.params)
         self.trace_cap = 1 << 14
         self.last_trace = None
         self.geometry = launch_geometry(kernel, env.params)
@@ -201,6 +209,10 @@ class GenericLauncher:
 
     def launch(self, env=None, stream=None):
         env = env or self.env
+        if env is not self.env and temp_params(self.kernel):
+            # temporaries sized by parameters: the program of these values
+            self.program = program_for(self.kernel, self.program.checked,
+                                       self.program.trace, env.params)
         prog = self.program
         dev = env.device if env.device is not None else torch.device(
             "cuda", torch.cuda.current_device())

@@ -301,3 +301,46 @@ def test_generic_wide_build_past_2_31(cuda):
     idx = torch.tensor([0, (1 << 31) - 1, 1 << 31, n - 1], device=cuda)
     assert bool((out[idx] == 0.75).all())
     assert int((out != 0.75).sum()) == 0
+
+
+REV_F = """subroutine rev(y, x, n)
+  implicit none
+  real*8 y(n), x(n), t(n)
+  integer n, i
+
+  do i = 1, n
+    t(i) = 2*x(i)
+  end do
+  do i = 1, n
+    y(i) = t(n + 1 - i) + x(i)
+  end do
+end
+"""
+
+
+def test_temporaries_sized_by_parameters_compile():
+    """A local array sized by a parameter (the reference allocates it from
+    the call's parameters, interp.py:332-338): the program is specialised
+    to the launch's values; without values it is a CodegenError."""
+    _raw, knl = fx.translate(REV_F)
+    with pytest.raises(CodegenError, match="symbolic extent"):
+        emit_cuda(knl)
+    for n in (5, 300):
+        prog = emit_cuda(knl, params={"n": n})
+        assert f"double t[{n}];" in prog.source
+        assert compile_program(prog, True)[:4] == b"\x7fELF"
+    with pytest.raises(CodegenError, match="budget"):
+        emit_cuda(knl, params={"n": 1 << 20})
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n", [5, 37, 300])
+def test_temporaries_sized_by_parameters_run(cuda, n):
+    from paper_1503_07659_b200._loopforge import interp
+    _raw, knl = fx.translate(REV_F)
+    x = np.random.default_rng(n).random(n)
+    ref = interp.interpret(knl, interp.make_env(knl, {"n": n}, {"x": x}))
+    env = lfb.make_device_env(knl, {"n": n}, {"x": x}, device=cuda)
+    out = lfb.interpret(knl, env)
+    assert lfb.get_output(out, "y").tobytes() == \
+        interp.get_output(ref, "y").tobytes()
