@@ -102,6 +102,15 @@ __device__ __forceinline__ void bulk_g2s_stream(void *dst, const void *src,
       : "memory");
 }
 
+// L2 prefetch of [src, src + bytes) through the TMA engine (no smem, no
+// completion): src 16-byte aligned, bytes a multiple of 16
+__device__ __forceinline__ void bulk_prefetch_l2(const void *src,
+                                                 uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src),
+               "r"(bytes)
+               : "memory");
+}
+
 __device__ __forceinline__ uint64_t policy_evict_first() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;"

@@ -607,6 +607,14 @@ static int sem_dispatch(double *w, const double *u, const double *d,
                                    grid_out);
     if (rc != -1) return rc;
   }
+  if ((var0 >= 70 && var0 <= 72) || (var0 == 0 && n == 16)) {
+    // line owners for phase 1 (semlap_line.cu), n = 9..16; the bitwise
+    // default at n = 16 (+10 % over the k-slab kernel, which stays the
+    // default below: n = 12..15 measured slower with line owners)
+    const int rc = sem_line_dispatch(n, var0 == 0 ? 70 : var0, w, u, d, g,
+                                     nelt, geom, s, grid_out);
+    if (rc != -1) return rc;
+  }
   if (var0 == 60 || var0 == 61 ||
       (var0 == 50 && (n == 9 || n == 10))) {
     // two k-columns per thread (semlap_gen2.cu), n = 7, 9..12; the DFMA-mode

@@ -1,6 +1,8 @@
 // Pieces shared by the two SEM kernels: the fused verification-norm epilogue.
 #pragma once
 
+#include <cuda.h>
+
 #include "lfb_common.cuh"
 
 namespace lfb {
@@ -89,6 +91,16 @@ int sem_kc_dispatch(int n, int variant, double *w, const double *u,
                     const double *d, const double *g, int64_t nelt,
                     const lfb_launch *geom, cudaStream_t s,
                     int64_t *grid_out);
+
+// -1 when the line-owner kernel has no entry for (n, variant)
+int sem_line_dispatch(int n, int variant, double *w, const double *u,
+                      const double *d, const double *g, int64_t nelt,
+                      const lfb_launch *geom, cudaStream_t s,
+                      int64_t *grid_out);
+
+// u of n = 16 elements as a (16 x 256 nelt) 2-D tensor map with the 128-B
+// swizzle (semlap_tc.cu); false when it cannot be encoded
+bool sem_u16_map(CUtensorMap *map, const double *u, int64_t nelt);
 
 int sem_slab_dispatch(int n, int variant, double *w, const double *u, const double *d,
                       const double *g, int64_t nelt, const lfb_launch *geom,

@@ -615,7 +615,7 @@ __global__ void __launch_bounds__(G *TcCfg<N>::T, 1)
 }
 
 // the (16 x rows) view of u for the swizzled staging (n = 16)
-static bool make_u_map(CUtensorMap *map, const double *u, int64_t nelt) {
+bool sem_u16_map(CUtensorMap *map, const double *u, int64_t nelt) {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
     void *p = nullptr;
     cudaDriverEntryPointQueryResult q;
@@ -682,7 +682,7 @@ static int launch_tc2(double *w, const double *u, const double *d,
   alignas(64) CUtensorMap umap;
   memset(&umap, 0, sizeof(umap));
   const bool swz = N == 16 && !(geom && geom->variant == 54) &&
-                   make_u_map(&umap, u, nelt);
+                   sem_u16_map(&umap, u, nelt);
   const size_t bytes = swz ? LS::total : L::total;
   {
     // two rotating constant slots per order (rows N and N + 10): one ring

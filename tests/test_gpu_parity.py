@@ -143,6 +143,17 @@ def test_semlap_slab_variants(cuda, n, variant):
                variant=variant, seed=variant + n)
 
 
+@pytest.mark.parametrize("n,variant", [(n, v) for n in range(9, 17)
+                                       for v in (70, 72)])
+@pytest.mark.parametrize("nelt", [1, 53, 300])
+def test_semlap_line_kernel(cuda, n, variant, nelt):
+    """Line-owner kernel (semlap_line.cu): phase 1 by the owners of the
+    u lines, bitwise; one element, a partial last round of groups, and
+    enough elements that every group wraps the slice ring several times."""
+    _sem_check(n, nelt, fx.semlap_source(n, block=1), cuda, [(0, nelt)],
+               variant=variant, seed=variant + n + nelt)
+
+
 @pytest.mark.parametrize("n", [3, 4, 5, 6, 7, 9, 10, 11])
 def test_semlap_slab_kernel_small_orders(cuda, n):
     """Variant 9 forces the k-slab kernel for orders the chunk kernel
@@ -173,7 +184,8 @@ def test_semlap_ragged_and_guarded(cuda, block, nelt):
 @pytest.mark.parametrize("n,variant", [(n, 50) for n in range(2, 17)]
                          + [(n, 51) for n in range(9, 17)]
                          + [(n, 61) for n in (7, 9, 10, 11, 12)]
-                         + [(n, 52) for n in range(7, 17)] + [(8, 53),
+                         + [(n, 52) for n in range(7, 17)]
+                         + [(n, 71) for n in range(9, 17)] + [(8, 53),
                                                               (8, 55),
                                                               (16, 54)])
 def test_semlap_fma_mode(cuda, n, variant):

@@ -159,7 +159,9 @@ if __name__ == "__main__":
         oks += [sem(8, 37, 0), sem(8, 37, 50, False), sem(8, 37, 39),
                 sem(4, 33, 0), sem(7, 9, 61, False), sem(9, 5, 0),
                 sem(12, 5, 0), sem(15, 3, 51, False), sem(16, 3, 51, False),
-                sem(16, 5, 52, False), sem(16, 5, 54, False)]
+                sem(16, 5, 52, False), sem(16, 5, 54, False),
+                sem(16, 7, 0), sem(13, 7, 70), sem(12, 4, 71, False),
+                sem(15, 3, 72)]
     if which in ("all", "gemm"):
         oks += [gemm("f32", 256, 256, 64, 0, False),
                 gemm("f32", 100, 60, 33, 1, True),
