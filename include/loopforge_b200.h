@@ -133,7 +133,9 @@ int64_t lfb_semlap_workspace(int npts, int nelt, const lfb_launch *geom);
  * the copies, write back and into plane_out (the upper rank of an
  * interface); 3: write plane_in into the copies.  Modes 1-3 take one
  * element plane (zlo == zhi, a multiple of n-1).  Deterministic; bitwise
- * the single-domain result when the ranks chain modes 1 -> 2 -> 3. */
+ * the single-domain result when the ranks chain modes 1 -> 2 -> 3.  Bits
+ * 4 and up of mode select a kernel variant (tuning; 0 = the default, every
+ * variant bitwise equal). */
 int lfb_dssum_f64(double *w, int n, int ex, int ey, int ez, int zlo,
                   int zhi, int mode, const double *plane_in,
                   double *plane_out, lfb_stream stream);
