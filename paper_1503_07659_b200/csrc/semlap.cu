@@ -607,10 +607,11 @@ static int sem_dispatch(double *w, const double *u, const double *d,
                                    grid_out);
     if (rc != -1) return rc;
   }
-  if ((var0 >= 70 && var0 <= 72) || (var0 == 0 && n == 16)) {
+  if ((var0 >= 70 && var0 <= 73) ||
+      (var0 == 0 && (n == 13 || n == 15 || n == 16))) {
     // line owners for phase 1 (semlap_line.cu), n = 9..16; the bitwise
-    // default at n = 16 (+10 % over the k-slab kernel, which stays the
-    // default below: n = 12..15 measured slower with line owners)
+    // default at n = 13, 15, 16 (+10..13 % over the k-slab kernel, which
+    // stays the default at n = 12, 14: equal there)
     const int rc = sem_line_dispatch(n, var0 == 0 ? 70 : var0, w, u, d, g,
                                      nelt, geom, s, grid_out);
     if (rc != -1) return rc;

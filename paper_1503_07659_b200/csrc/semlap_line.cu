@@ -68,16 +68,18 @@ struct LineCfg {
   static constexpr int SLAB = 6 * N2;               // g of one k-slice
 };
 
-template <int N, int G, bool USW>
+template <int N, int G, bool USW, int SD = 1>
 struct LineSmem {
   using C = LineCfg<N>;
   static constexpr int UST = USW ? C::NP : (C::NP + 2 + 1) / 2 * 2;
   static constexpr int SGU = UST / C::SLAB;  // g slots inside ua
-  static constexpr int S = (1 + SGU) < N ? 1 + SGU : N;
+  // SD dedicated slots (prefetched for the next element during phase 2 and
+  // phase 1), then the slots inside the dead u stage
+  static constexpr int S = (SD + SGU) < N ? SD + SGU : N;
   static constexpr size_t align = USW ? 1024 : 128;
   static constexpr size_t ua_off = 0;
   static constexpr size_t gd_off = ((size_t)UST * 8 + 127) / 128 * 128;
-  static constexpr size_t rr_off = gd_off + (size_t)C::SLAB * 8;
+  static constexpr size_t rr_off = gd_off + (size_t)SD * C::SLAB * 8;
   static constexpr size_t ss_off = rr_off + (size_t)C::RS * 8;
   static constexpr size_t grp_bytes =
       (ss_off + (size_t)C::RS * 8 + align - 1) / align * align;
@@ -121,7 +123,7 @@ __device__ __forceinline__ void line_contract(const double (&in)[N],
   }
 }
 
-template <int N, int G, bool USW, bool SUMSQ, bool F, bool PF>
+template <int N, int G, bool USW, bool SUMSQ, bool F, bool PF, int SD>
 __global__ void __launch_bounds__(G *LineCfg<N>::T, 1)
     semlap_line_kernel(double *__restrict__ w, const double *__restrict__ u,
                        const double *__restrict__ d,
@@ -129,10 +131,12 @@ __global__ void __launch_bounds__(G *LineCfg<N>::T, 1)
                        double *__restrict__ partials,
                        const __grid_constant__ CUtensorMap umap) {
   using C = LineCfg<N>;
-  using L = LineSmem<N, G, USW>;
+  using L = LineSmem<N, G, USW, SD>;
   constexpr int N2 = C::N2, NP = C::NP, T = C::T, S = L::S;
+  static_assert(SD >= 1 && SD <= S, "dedicated slots");
+  constexpr bool UTC = N < 16;  // ut contracted inside the combine
   static_assert(N >= 9 && N <= 16, "n = 9..16");
-  static_assert(G * (1 + S) <= 64 && G <= 15, "mbarriers, barrier ids");
+  static_assert(G * (1 + S) <= 63 && G <= 15, "mbarriers, barrier ids");
   static_assert(!USW || N == 16, "swizzled u staging: 128-B rows");
 
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -156,9 +160,10 @@ __global__ void __launch_bounds__(G *LineCfg<N>::T, 1)
   double *rr = reinterpret_cast<double *>(gbase + L::rr_off);
   double *ss = reinterpret_cast<double *>(gbase + L::ss_off);
   uint64_t *ubar = bars + grp * (1 + S);
+  uint64_t *zero = bars + 63;  // holds 0 (see phase 2)
   uint64_t *gbar = ubar + 1;
   auto slot_ptr = [&](int s) -> double * {
-    return s == 0 ? gd : ua + (size_t)(s - 1) * C::SLAB;
+    return s < SD ? gd + (size_t)s * C::SLAB : ua + (size_t)(s - SD) * C::SLAB;
   };
 
   const int64_t q0 = (int64_t)blockIdx.x * G + grp;
@@ -168,6 +173,7 @@ __global__ void __launch_bounds__(G *LineCfg<N>::T, 1)
 
   if (tid == 0) {
     for (int x = 0; x < G * (1 + S); ++x) mbar_init(&bars[x], 1);
+    *zero = 0;
     fence_mbar_init();
   }
   for (int x = tid; x < N2; x += G * T) dn[(x / N) + N * (x % N)] = d[x];
@@ -215,7 +221,7 @@ __global__ void __launch_bounds__(G *LineCfg<N>::T, 1)
 
   if (lt == 0 && mine > 0) {
     issue_u(0);
-    issue_slice(0, 0);
+    for (int k = 0; k < SD; ++k) issue_slice(0, k);
   }
 
   double acc_sq = 0.0;
@@ -239,7 +245,7 @@ __global__ void __launch_bounds__(G *LineCfg<N>::T, 1)
     }
 
     // ---- phase 1: the thread's three lines
-    double ut[N];
+    double uc[N];
     if (active) {
       double in[N], out[N];
       // i-line u(:, a, b), row R = lt
@@ -270,15 +276,23 @@ __global__ void __launch_bounds__(G *LineCfg<N>::T, 1)
       line_contract<N, F>(in, out);
 #pragma unroll
       for (int x = 0; x < N; ++x) ss[line_ridx<N>(ta, x + N * tb)] = out[x];
-      // k-line u(a, b, :): rows b + N l
+      // k-line u(a, b, :): rows b + N l.  UTC: kept, its contraction runs
+      // slice by slice inside the combine where it hides the g-slice
+      // latency (n < 16: +1..13 %); n = 16: contracted here (inside the
+      // combine ptxas spilled phase 2 under the 128-register cap)
 #pragma unroll
-      for (int l = 0; l < N; ++l) in[l] = ust[line_uidx<N, USW>(ta, tb + N * l)];
-      line_contract<N, F>(in, ut);
+      for (int l = 0; l < N; ++l) uc[l] = ust[line_uidx<N, USW>(ta, tb + N * l)];
+      if constexpr (!UTC) {
+        double t[N];
+        line_contract<N, F>(uc, t);
+#pragma unroll
+        for (int l = 0; l < N; ++l) uc[l] = t[l];  // uc now holds ut
+      }
     }
     named_bar_sync(1 + grp, T);  // u read by all; ur / us complete
     if (lt == 0) {
       fence_proxy_async_smem();
-      for (int k = 1; k < S; ++k) issue_slice(m, k);  // slots inside ua
+      for (int k = SD; k < S; ++k) issue_slice(m, k);  // slots inside ua
     }
 
     // ---- combine with g, slice by slice: wr / ws in place, wt in registers
@@ -293,18 +307,27 @@ __global__ void __launch_bounds__(G *LineCfg<N>::T, 1)
         const double2 g01 = g2[0], g23 = g2[1], g45 = g2[2];
         const int x = line_ridx<N>(ta, tb + N * k);
         const double ur = rr[x], us = ss[x];
-        rr[x] = comb3<F>(g01.x, ur, g01.y, us, g23.x, ut[k]);
-        ss[x] = comb3<F>(g01.y, ur, g23.y, us, g45.x, ut[k]);
-        wt[k] = comb3<F>(g23.x, ur, g45.x, us, g45.y, ut[k]);
+        // ut(i, j, k) = sum_l d(k, l) u(i, j, l), l ascending
+        double ut;
+        if constexpr (UTC) {
+          ut = mac0<F>(LINE_D(k), uc[0]);
+#pragma unroll
+          for (int l = 1; l < N; ++l) ut = mac<F>(ut, LINE_D(k + N * l), uc[l]);
+        } else {
+          ut = uc[k];
+        }
+        rr[x] = comb3<F>(g01.x, ur, g01.y, us, g23.x, ut);
+        ss[x] = comb3<F>(g01.y, ur, g23.y, us, g45.x, ut);
+        wt[k] = comb3<F>(g23.x, ur, g45.x, us, g45.y, ut);
       }
       named_bar_sync(1 + grp, T);  // slot s consumed (last: wr/ws complete)
       if (lt == 0) {
         if (k + S < N) {
           fence_proxy_async_smem();
           issue_slice(m, k + S);
-        } else if (s == 0 && m + 1 < mine) {
+        } else if (s < SD && m + 1 < mine) {
           fence_proxy_async_smem();
-          issue_slice(m + 1, 0);
+          issue_slice(m + 1, s);  // dedicated: the next element's first
         }
         if (k == N - 1 && m + 1 < mine) {
           fence_proxy_async_smem();
@@ -324,10 +347,20 @@ __global__ void __launch_bounds__(G *LineCfg<N>::T, 1)
       for (int l = 0; l < N; l += 2) {
         constexpr int H = 2;
         double da[H], db[H];  // d(l + h, i), d(l + h, j)
+        // wt(l) XOR a zero from a volatile shared load, per l pair
+        // (bit-exact): ptxas would otherwise compute all n^2 products
+        // d(l, k) wt(l) up front and spill them
+        uint64_t z;
+        asm volatile("ld.volatile.shared.u64 %0, [%1];"
+                     : "=l"(z)
+                     : "r"(smem_u32(zero)));
 #pragma unroll
         for (int h = 0; h < H; ++h)
-          if (l + h < N)
+          if (l + h < N) {
             da[h] = dn[ta + N * (l + h)], db[h] = dn[tb + N * (l + h)];
+            wt[l + h] = __longlong_as_double(
+                __double_as_longlong(wt[l + h]) ^ (long long)z);
+          }
 #pragma unroll
         for (int k = 0; k < N; ++k) {
           const int rrow = tb + N * k;  // wr(:, j, k)
@@ -361,22 +394,22 @@ __global__ void __launch_bounds__(G *LineCfg<N>::T, 1)
   if constexpr (SUMSQ) block_sumsq_partial(acc_sq, partials);
 }
 
-template <int N, int G, bool USW, bool F, bool PF>
+template <int N, int G, bool USW, bool F, bool PF, int SD>
 static void line_launch(bool sumsq, int grid, double *w, const double *u,
                         const double *d, const double *g, int64_t nelt,
                         const lfb_launch *geom, const CUtensorMap &umap,
                         cudaStream_t s) {
-  using L = LineSmem<N, G, USW>;
+  using L = LineSmem<N, G, USW, SD>;
   static_assert(L::total <= 227 * 1024, "smem");
-  auto k = sumsq ? semlap_line_kernel<N, G, USW, true, F, PF>
-                 : semlap_line_kernel<N, G, USW, false, F, PF>;
+  auto k = sumsq ? semlap_line_kernel<N, G, USW, true, F, PF, SD>
+                 : semlap_line_kernel<N, G, USW, false, F, PF, SD>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)L::total);
   k<<<grid, G * LineCfg<N>::T, L::total, s>>>(
       w, u, d, g, nelt, sumsq ? geom->workspace : nullptr, umap);
 }
 
-template <int N, int G, bool F, bool PF = true>
+template <int N, int G, bool F, int SD = 1, bool PF = true>
 static int launch_line(double *w, const double *u, const double *d,
                        const double *g, int64_t nelt, const lfb_launch *geom,
                        cudaStream_t s, int64_t *grid_out) {
@@ -404,11 +437,11 @@ static int launch_line(double *w, const double *u, const double *d,
                                 &capturing))
       return rc;
     if (usw)
-      line_launch<N, G, N == 16, F, PF>(sumsq, grid, w, u, d, g, nelt, geom,
-                                    umap, s);
+      line_launch<N, G, N == 16, F, PF, SD>(sumsq, grid, w, u, d, g, nelt,
+                                            geom, umap, s);
     else
-      line_launch<N, G, false, F, PF>(sumsq, grid, w, u, d, g, nelt, geom, umap,
-                                  s);
+      line_launch<N, G, false, F, PF, SD>(sumsq, grid, w, u, d, g, nelt,
+                                          geom, umap, s);
     dconst_release(3, slot, s, capturing);
   }
   if (int rc = check_launch("lfb_semlap_f64(line)")) return rc;
@@ -416,29 +449,36 @@ static int launch_line(double *w, const double *u, const double *d,
                : LFB_OK;
 }
 
-// (n, variant) -> groups per CTA.  70: bitwise, 71: the same in DFMA mode,
-// 72 / 73: bitwise with another group count
-#define LFB_LINE_TABLE(X) \
-  X(9, 4, 6)              \
-  X(10, 4, 6)             \
-  X(11, 3, 4)             \
-  X(12, 3, 4)             \
-  X(13, 2, 3)             \
-  X(14, 2, 3)             \
-  X(15, 2, 1)             \
-  X(16, 2, 1)
+// (n, variant) -> (groups per CTA, dedicated g slots).  70: bitwise, 71:
+// the same in DFMA mode, 72: bitwise with (GB, SDB), 73: bitwise with one
+// dedicated slot (the first ring)
+#define LFB_LINE_TABLE(X)  \
+  X(9, 4, 3, 6, 1)         \
+  X(10, 4, 3, 6, 1)        \
+  X(11, 3, 4, 4, 1)        \
+  X(12, 3, 4, 4, 1)        \
+  X(13, 2, 7, 3, 1)        \
+  X(14, 2, 4, 3, 1)        \
+  X(15, 2, 1, 1, 1)        \
+  X(16, 2, 1, 1, 1)
 
 int sem_line_dispatch(int n, int variant, double *w, const double *u,
                       const double *d, const double *g, int64_t nelt,
                       const lfb_launch *geom, cudaStream_t s,
                       int64_t *grid_out) {
-#define X(NN, GA, GB)                                                        \
+#define X(NN, GA, SA, GB, SB)                                                \
   if (n == NN && variant == 70)                                              \
-    return launch_line<NN, GA, false>(w, u, d, g, nelt, geom, s, grid_out);  \
+    return launch_line<NN, GA, false, SA>(w, u, d, g, nelt, geom, s,         \
+                                          grid_out);                         \
   if (n == NN && variant == 71)                                              \
-    return launch_line<NN, GA, true>(w, u, d, g, nelt, geom, s, grid_out);   \
+    return launch_line<NN, GA, true, SA>(w, u, d, g, nelt, geom, s,          \
+                                         grid_out);                          \
   if (n == NN && variant == 72)                                              \
-    return launch_line<NN, GB, false>(w, u, d, g, nelt, geom, s, grid_out);
+    return launch_line<NN, GB, false, SB>(w, u, d, g, nelt, geom, s,         \
+                                          grid_out);                         \
+  if (n == NN && variant == 73)                                              \
+    return launch_line<NN, GA, false, 1>(w, u, d, g, nelt, geom, s,          \
+                                         grid_out);
   LFB_LINE_TABLE(X)
 #undef X
   return -1;
