@@ -725,3 +725,40 @@ def test_semlap_offsets_past_2_31(cuda, variant):
             mag = oracle.semlap(np.zeros(np3), np.abs(ue), np.abs(dh),
                                 np.abs(ge), n, 1)
             assert (np.abs(we - ref) <= 1e-12 * mag).all(), e
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,variant", [(16, 0), (15, 0), (13, 0), (16, 50)])
+def test_semlap_high_order_offsets_past_2_31(cuda, n, variant):
+    """The high-order defaults (line-owner kernel bitwise, DMMA kernel in
+    DFMA mode) past the 2^31 flat index of g: nelt just above
+    2^31 / (6 n^3), every element written, sampled elements around the
+    boundary, the ends and random places against the oracle."""
+    np3 = n ** 3
+    cross = (1 << 31) // (6 * np3)
+    nelt = cross + 53
+    _raw, knl = fx.translate(fx.semlap_source(n, block=1))
+    u, d, g = _sem_inputs(n, nelt, cuda, 78 + n)
+    w = torch.full_like(u, float("nan"))
+    env = lfb.env_from_buffers(knl, {"nelt": nelt},
+                               {"u": u, "d": d, "g": g, "w": w})
+    lfb.interpret(knl, env, inplace=True, variant=variant)
+    torch.cuda.synchronize()
+    assert not bool(torch.isnan(w).any())
+    es = np.unique(np.concatenate([
+        [0, 1, nelt - 2, nelt - 1, cross - 1, cross, cross + 1],
+        np.random.default_rng(n).integers(0, nelt, 24)]))
+    dh = d.cpu().numpy()
+    for e in es.tolist():
+        ue = u[e * np3:(e + 1) * np3].cpu().numpy()
+        ge = g[6 * e * np3:6 * (e + 1) * np3].cpu().numpy()
+        we = w[e * np3:(e + 1) * np3].cpu().numpy()
+        ref = oracle.semlap(np.zeros(np3), ue, dh, ge, n, 1)
+        if variant == 0:
+            assert we.tobytes() == ref.tobytes(), e
+        else:
+            mag = oracle.semlap(np.zeros(np3), np.abs(ue), np.abs(dh),
+                                np.abs(ge), n, 1)
+            assert (np.abs(we - ref) <= 1e-12 * mag).all(), e
+    del u, d, g, w, env
+    torch.cuda.empty_cache()
