@@ -153,6 +153,29 @@ def test_device_dssum_matches_the_oracle(cuda, mesh):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("n", list(range(2, 17)))
+def test_device_dssum_every_order(cuda, n):
+    """The default kernel is instantiated per order (p a compile-time
+    constant): every n = 2..16 on a ragged box, whole mesh and a Z range,
+    bitwise against the oracle."""
+    from paper_1503_07659_b200.assembly import _launch, dssum
+    mesh = BoxMesh(3, 2, 4, n)
+    w = _field(mesh, n)
+    d = torch.from_numpy(w).to(cuda)
+    dssum(d, mesh)
+    want = oracle.dssum(w.copy(), n, mesh.ex, mesh.ey, mesh.ez)
+    assert d.cpu().numpy().tobytes() == want.tobytes()
+    # a Z sub-range (as a rank's interior layers): the oracle over the same
+    # range
+    zlo, zhi = 1, mesh.top - 1
+    d = torch.from_numpy(w).to(cuda)
+    _launch(d, mesh, zlo, zhi, 0)
+    want = oracle.dssum(w.copy(), n, mesh.ex, mesh.ey, mesh.ez, zlo=zlo,
+                        zhi=zhi)
+    assert d.cpu().numpy().tobytes() == want.tobytes()
+
+
+@pytest.mark.gpu
 def test_device_dssum_modes_chain(cuda):
     """Modes 1 -> 2 -> 3 on two slabs of one mesh (in one process) give the
     single-domain kernel's bits."""
