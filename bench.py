@@ -207,6 +207,43 @@ def sem_buffers(n, nelt, dev, seed):
     return u, d, g, w
 
 
+def _sem_sample_check(u, g, d, w, n, nelt, exact, count=1024, seed=7):
+    """Elements 0, 1, nelt - 1 and *count* random ones across the whole
+    range, gathered from the device and checked against the oracle: bitwise
+    (*exact*), else per point within 1e-12 of the magnitude of the summed
+    terms (the same operator on |u|, |d|, |g|)."""
+    import numpy as np
+    import torch
+    sys.path.insert(0, os.path.join(REPO, "oracle"))
+    import oracle
+    np3 = n ** 3
+    es = np.unique(np.concatenate([
+        [0, 1, nelt - 1],
+        np.random.default_rng(seed).integers(0, nelt, count)]))
+    idx = torch.as_tensor(es, device=u.device)
+
+    def gather(t, per):
+        return t.view(-1, per).index_select(0, idx).reshape(-1).cpu() \
+            .numpy()
+    uh, gh, wh = gather(u, np3), gather(g, 6 * np3), gather(w, np3)
+    dh = d.cpu().numpy()
+    ref = oracle.semlap(np.zeros_like(uh), uh, dh, gh, n, len(es),
+                        threads=8)
+    out = {"elements": int(len(es)), "spread": "0, 1, last and random "
+           "elements across the whole range"}
+    if exact:
+        out["bitwise"] = bool(wh.tobytes() == ref.tobytes())
+        out["pass"] = out["bitwise"]
+    else:
+        mag = oracle.semlap(np.zeros_like(uh), np.abs(uh), np.abs(dh),
+                            np.abs(gh), n, len(es), threads=8)
+        err = float((np.abs(wh - ref) / mag).max())
+        out["max_err_over_magnitude"] = err
+        out["tolerance"] = 1e-12
+        out["pass"] = err <= 1e-12
+    return out
+
+
 def sem_bench(args, rank, world, local):
     import numpy as np
     import torch
@@ -242,6 +279,12 @@ def sem_bench(args, rank, world, local):
                    "ms_per_step": ms_b,
                    "roofline_frac": 64 * np3 * nelt / (ms_b_local * 1e-3)
                    / 1e9 / _peaks()[0], "clocks": clocks_b}
+        if not args.no_verify:
+            # w holds the bitwise kernel's result: head, tail and random
+            # elements across the whole shard, bitwise against the oracle
+            torch.cuda.synchronize()
+            bitwise["verify"] = _sem_sample_check(u, g, d, w, n, nelt,
+                                                  exact=True)
     value = nelt_total * np3 / (ms * 1e-3) / 1e9
     bytes_per_launch = 64 * np3 * nelt
     achieved = bytes_per_launch / (ms_local * 1e-3) / 1e9
@@ -297,6 +340,8 @@ def sem_bench(args, rank, world, local):
                     (np.abs(got - ref) / mag).max())
         if sem_variant == 50:
             verify["tolerance"] = 1e-12
+        verify["sampled"] = _sem_sample_check(u, g, d, w, n, nelt,
+                                              exact=sem_variant != 50)
 
     res = {
         "metric": METRIC, "value": value, "unit": "GDOF/s",
