@@ -479,11 +479,18 @@ __global__ void __launch_bounds__(G *TcCfg<N>::T, 1)
     for (int64_t x = 0; x < SGS && x < nslabs; ++x) issue_slab(x);
   }
 
+  // the contraction index of the phase-1 products for k-step ks, lane q:
+  // 4 ks + q, or for odd n with four k-steps (13, 15) 4 q + ks -- then the
+  // four q of a half warp read u rows 4 apart, and N x {0, 4, 8, 12} hits
+  // four different bank quarters for odd N (the plain order was 2-way
+  // conflicted in both fragment loads, ncu source view)
+  constexpr bool RHO = KT == 4 && (N % 2 == 1);
+  auto lk = [&](int ks) -> int { return RHO ? 4 * q + ks : 4 * ks + q; };
   double fa_r[KT], fb_s[KT], fa_t[KT], fb_t[KT];
 #pragma unroll
   for (int ks = 0; ks < KT; ++ks) {
-    fa_r[ks] = dtc<N, ROW>(8 * it + r, 4 * ks + q);
-    fb_s[ks] = dtc<N, ROW>(8 * jt + r, 4 * ks + q);
+    fa_r[ks] = dtc<N, ROW>(8 * it + r, lk(ks));
+    fb_s[ks] = dtc<N, ROW>(8 * jt + r, lk(ks));
     fa_t[ks] = dtc<N, ROW>(4 * ks + q, 8 * it + r);
     fb_t[ks] = dtc<N, ROW>(4 * ks + q, 8 * jt + r);
   }
@@ -527,10 +534,10 @@ __global__ void __launch_bounds__(G *TcCfg<N>::T, 1)
       double r0 = 0.0, r1 = 0.0, s0 = 0.0, s1 = 0.0;
 #pragma unroll
       for (int ks = 0; ks < KT; ++ks) {
-        dmma(r0, r1, ust[uidx<N, SWZ>(4 * ks + q, 8 * jt + r + N * k)],
+        dmma(r0, r1, ust[uidx<N, SWZ>(lk(ks), 8 * jt + r + N * k)],
              fa_r[ks]);
         dmma(s0, s1, fb_s[ks],
-             ust[uidx<N, SWZ>(8 * it + r, 4 * ks + q + N * k)]);
+             ust[uidx<N, SWZ>(8 * it + r, lk(ks) + N * k)]);
       }
       if (k % KS == 0)
         mbar_wait(&gbar[(s / KS) % SGS], (uint32_t)((s / KS / SGS) & 1));
