@@ -8,10 +8,11 @@
 //  * default (tensor cores, tolerance parity): the FP64 DMMA units
 //    (mma.sync m8n8k4 f64), acc = sum_k a(i,k) b(k,j) fused in the tensor
 //    pipe, then c = c + alpha*acc -- within the north star's 1e-12 relative
-//    fp64 bound normwise (tests/test_gpu_parity.py).  128x128x16 CTA tiles
-//    through a 4-stage cp.async ring in padded shared memory (row strides
-//    132 and 20 doubles: every fragment load of a half warp hits 16
-//    distinct 8-byte bank slots), 8 warps of 64x32 each: per k-step of 4,
+//    fp64 bound normwise (tests/test_gpu_parity.py).  128x128x32 CTA tiles
+//    through a 3-stage cp.async ring (128x128x16 x 4 stages when l is not a
+//    multiple of 32) in padded shared memory (row strides 132 and BK + 4
+//    doubles: every fragment load of a half warp hits 16 distinct 8-byte
+//    bank slots), 8 warps of 64x32 each: per k-step of 4,
 //    8 A and 4 B fragment loads feed 32 DMMAs.  Needs m, n % 128 == 0,
 //    l % 16 == 0 and 16-byte aligned arrays; other shapes take the exact
 //    kernel.
@@ -27,13 +28,14 @@ namespace lfb {
 constexpr int DG_BM = 128, DG_BN = 128, DG_BK = 16, DG_STAGES = 4;
 constexpr int DG_THREADS = 256;
 constexpr int DG_AS = 132;  // As row stride (doubles): k rows of 128 i
-constexpr int DG_BS = 20;   // Bs row stride: j rows of 16 k
 
+template <int BK, int ST>
 struct DgSmem {
-  static constexpr size_t a_doubles = DG_BK * DG_AS;
-  static constexpr size_t b_doubles = DG_BN * DG_BS;
+  static constexpr int BS = BK + 4;  // Bs row stride: j rows of BK k
+  static constexpr size_t a_doubles = BK * DG_AS;
+  static constexpr size_t b_doubles = DG_BN * BS;
   static constexpr size_t stage = a_doubles + b_doubles;
-  static constexpr size_t total = DG_STAGES * stage * 8;
+  static constexpr size_t total = ST * stage * 8;
 };
 
 __device__ __forceinline__ void dg_dmma(double &d0, double &d1, double a,
@@ -52,32 +54,36 @@ __device__ __forceinline__ void cp16(void *dst, const void *src) {
                : "memory");
 }
 
+// BK k per stage, ST stages
+template <int BK, int ST>
 __global__ void __launch_bounds__(DG_THREADS, 1)
     dgemm_dmma_kernel(double alpha, const double *__restrict__ a,
                       const double *__restrict__ b, double *__restrict__ c,
                       int l, int m, int n) {
+  using L = DgSmem<BK, ST>;
+  constexpr int BS = L::BS, KS = BK / 4;
   extern __shared__ __align__(128) double dsm[];
   const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
   const int r = lane / 4, q = lane % 4;
   const int wm = warp / 4, wn = warp % 4;  // 2 x 4 warps of 64 x 32
   const int i0 = blockIdx.x * DG_BM, j0 = blockIdx.y * DG_BN;
-  const int nk = l / DG_BK;
+  const int nk = l / BK;
 
-  auto As = [&](int s) { return dsm + (size_t)s * DgSmem::stage; };
-  auto Bs = [&](int s) { return As(s) + DgSmem::a_doubles; };
+  auto As = [&](int s) { return dsm + (size_t)s * L::stage; };
+  auto Bs = [&](int s) { return As(s) + L::a_doubles; };
   auto load = [&](int s, int kt) {
-    const int k0 = kt * DG_BK;
+    const int k0 = kt * BK;
     double *as = As(s), *bs = Bs(s);
 #pragma unroll
-    for (int x = 0; x < 4; ++x) {
+    for (int x = 0; x < BK / 4; ++x) {
       const int ch = tid + DG_THREADS * x;
-      {  // A: 16 rows (k) of 128 i, 64 chunks of 2 doubles per row
+      {  // A: BK rows (k) of 128 i, 64 chunks of 2 doubles per row
         const int k = ch / 64, i = (ch % 64) * 2;
         cp16(as + k * DG_AS + i, a + (i0 + i) + (int64_t)m * (k0 + k));
       }
-      {  // B: 128 rows (j) of 16 k, 8 chunks per row
-        const int j = ch / 8, k = (ch % 8) * 2;
-        cp16(bs + j * DG_BS + k, b + (k0 + k) + (int64_t)l * (j0 + j));
+      {  // B: 128 rows (j) of BK k, BK / 2 chunks per row
+        const int j = ch / (BK / 2), k = (ch % (BK / 2)) * 2;
+        cp16(bs + j * BS + k, b + (k0 + k) + (int64_t)l * (j0 + j));
       }
     }
   };
@@ -89,28 +95,31 @@ __global__ void __launch_bounds__(DG_THREADS, 1)
     for (int nt = 0; nt < 4; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
 
 #pragma unroll
-  for (int s = 0; s < DG_STAGES - 1; ++s) {
+  for (int s = 0; s < ST - 1; ++s) {
     if (s < nk) load(s, s);
     asm volatile("cp.async.commit_group;" ::: "memory");
   }
   for (int kt = 0; kt < nk; ++kt) {
-    asm volatile("cp.async.wait_group %0;" ::"n"(DG_STAGES - 2) : "memory");
+    asm volatile("cp.async.wait_group %0;" ::"n"(ST - 2) : "memory");
     __syncthreads();  // stage kt landed for every thread; stage kt-1 free
     {
-      const int nxt = kt + DG_STAGES - 1;
-      if (nxt < nk) load(nxt % DG_STAGES, nxt);
+      const int nxt = kt + ST - 1;
+      if (nxt < nk) load(nxt % ST, nxt);
       asm volatile("cp.async.commit_group;" ::: "memory");
     }
-    const double *as = As(kt % DG_STAGES), *bs = Bs(kt % DG_STAGES);
-#pragma unroll
-    for (int ks = 0; ks < DG_BK / 4; ++ks) {
-      double fa[8], fb[4];
+    const double *as = As(kt % ST), *bs = Bs(kt % ST);
+    auto frags = [&](int ks, double (&fa)[8], double (&fb)[4]) {
 #pragma unroll
       for (int mt = 0; mt < 8; ++mt)  // A[i][k]: row i = lane/4, col k
         fa[mt] = as[(4 * ks + q) * DG_AS + wm * 64 + mt * 8 + r];
 #pragma unroll
       for (int nt = 0; nt < 4; ++nt)  // B[k][j]: row k = lane%4, col j
-        fb[nt] = bs[(wn * 32 + nt * 8 + r) * DG_BS + 4 * ks + q];
+        fb[nt] = bs[(wn * 32 + nt * 8 + r) * BS + 4 * ks + q];
+    };
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      double fa[8], fb[4];
+      frags(ks, fa, fb);
 #pragma unroll
       for (int mt = 0; mt < 8; ++mt)
 #pragma unroll
@@ -132,6 +141,19 @@ __global__ void __launch_bounds__(DG_THREADS, 1)
         double *p = c + i + (int64_t)m * j;
         *p = dadd(*p, dmul(alpha, acc[mt][nt][h]));
       }
+}
+
+template <int BK, int ST>
+static int launch_dgemm_dmma(double alpha, const double *a, const double *b,
+                             double *c, int l, int m, int n, cudaStream_t s) {
+  using L = DgSmem<BK, ST>;
+  static_assert(L::total <= 227 * 1024, "smem");
+  auto k = dgemm_dmma_kernel<BK, ST>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)L::total);
+  dim3 grid(m / DG_BM, n / DG_BN);
+  k<<<grid, DG_THREADS, L::total, s>>>(alpha, a, b, c, l, m, n);
+  return check_launch("lfb_dgemm_f64(dmma)");
 }
 
 // }}}
@@ -235,13 +257,12 @@ extern "C" int lfb_dgemm_f64(double alpha, const double *a, const double *b,
   const bool tc_ok = m % DG_BM == 0 && n % DG_BN == 0 && l % DG_BK == 0 &&
                      l > 0 && aligned(a, 16) && aligned(b, 16);
   if (variant != 1 && tc_ok) {
-    cudaFuncSetAttribute(dgemm_dmma_kernel,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)DgSmem::total);
-    dim3 grid(m / DG_BM, n / DG_BN);
-    dgemm_dmma_kernel<<<grid, DG_THREADS, DgSmem::total, s>>>(alpha, a, b, c,
-                                                             l, m, n);
-    return check_launch("lfb_dgemm_f64(dmma)");
+    // k tiles of 32 through 3 stages when l allows (half the ring barriers
+    // of 16 x 4: 31.3 vs 30.9 TFLOP/s at 8192^3); variant 3 forces 16 x 4.
+    // Double-buffering the fragment registers measured no gain.
+    if (variant != 3 && l % 32 == 0)
+      return launch_dgemm_dmma<32, 3>(alpha, a, b, c, l, m, n, s);
+    return launch_dgemm_dmma<DG_BK, DG_STAGES>(alpha, a, b, c, l, m, n, s);
   }
   if (variant == 2)
     return fail(LFB_ERR_UNSUPPORTED,

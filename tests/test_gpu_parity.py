@@ -572,9 +572,12 @@ def test_sgemm_tensor_cores(cuda, m, n, l, variant):
     assert err_exact <= 1e-5
 
 
-@pytest.mark.parametrize("m,n,l", [(128, 128, 16), (256, 384, 512),
-                                   (1024, 512, 2048), (512, 256, 8192)])
-def test_dgemm_tensor_cores(cuda, m, n, l):
+@pytest.mark.parametrize("m,n,l,variant", [(128, 128, 16, 0),
+                                           (256, 384, 512, 0),
+                                           (1024, 512, 2048, 0),
+                                           (512, 256, 8192, 0),
+                                           (256, 384, 512, 3)])
+def test_dgemm_tensor_cores(cuda, m, n, l, variant):
     """The paper's DGEMM in real*8 on the FP64 tensor cores (DMMA):
     tolerance parity (north star: 1e-12 relative fp64) against the
     reference's sequential-k result -- normwise, and per entry against the
@@ -589,7 +592,7 @@ def test_dgemm_tensor_cores(cuda, m, n, l):
         knl, {"m": m, "n": n, "l": l},
         {"a": torch.from_numpy(a).to(cuda), "b": torch.from_numpy(b).to(cuda),
          "c": torch.from_numpy(c.copy()).to(cuda)}, {"alpha": alpha})
-    out = lfb.interpret(knl, env)
+    out = lfb.interpret(knl, env, variant=variant)  # 3: 16 x 4 k tiles
     got = out.arrays["c"].data.cpu().numpy()
     ref = oracle.sgemm(alpha, a, b, c.copy(), l, m, n, threads=8)
     mag = oracle.sgemm(alpha, np.abs(a), np.abs(b), np.abs(c), l, m, n,
