@@ -23,6 +23,38 @@ __global__ void dmma_kernel(double *out, int iters) {
   if (s == 1.2345) out[0] = s;
 }
 
+// the dgemm kernel's issue pattern: an 8 x 4 grid of accumulators fed by 8
+// A and 4 B fragments (distinct registers, each reused 4 or 8 times)
+__global__ void dmma_grid_kernel(double *out, int iters) {
+  double fa[8], fb[4];
+#pragma unroll
+  for (int x = 0; x < 8; ++x) fa[x] = 1.0 + (threadIdx.x + x) * 1e-9;
+#pragma unroll
+  for (int x = 0; x < 4; ++x) fb[x] = 0.5 + (blockIdx.x + x) * 1e-9;
+  double c[8][4][2];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) c[i][j][0] = c[i][j][1] = (i + j) * 1e-3;
+  for (int it = 0; it < iters / 4; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        asm volatile(
+            "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, "
+            "{%3}, {%0,%1};"
+            : "+d"(c[i][j][0]), "+d"(c[i][j][1])
+            : "d"(fa[i]), "d"(fb[j]));
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) s += c[i][j][0] + c[i][j][1];
+  if (s == 1.2345) out[0] = s;
+}
+
 __global__ void dfma_kernel(double *out, int iters) {
   double a = 1.0 + threadIdx.x * 1e-9, b = 0.5 + blockIdx.x * 1e-9;
   double c[8];
@@ -58,6 +90,14 @@ int main() {
     double flops = 2.0 * 8 * 8 * 4 * 8.0 * iters * warps * sms;
     printf("DMMA m8n8k4 warps/SM %2d: %.2f TFLOP/s\n", warps,
            flops / (ms * 1e-3) / 1e12);
+    dmma_grid_kernel<<<sms, 32 * warps>>>(o, 16);
+    cudaEventRecord(e0);
+    dmma_grid_kernel<<<sms, 32 * warps>>>(o, iters);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    cudaEventElapsedTime(&ms, e0, e1);
+    printf("DMMA 8x4 grid (dgemm pattern) warps/SM %2d: %.2f TFLOP/s\n",
+           warps, flops / (ms * 1e-3) / 1e12);
     dfma_kernel<<<sms, 32 * warps>>>(o, 16);
     cudaEventRecord(e0);
     dfma_kernel<<<sms, 32 * warps>>>(o, iters);
