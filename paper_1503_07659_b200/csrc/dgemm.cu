@@ -9,10 +9,11 @@
 //    (mma.sync m8n8k4 f64), acc = sum_k a(i,k) b(k,j) fused in the tensor
 //    pipe, then c = c + alpha*acc -- within the north star's 1e-12 relative
 //    fp64 bound normwise (tests/test_gpu_parity.py).  128x128x32 CTA tiles
-//    through a 3-stage cp.async ring (128x128x16 x 4 stages when l is not a
-//    multiple of 32) in padded shared memory (row strides 132 and BK + 4
-//    doubles: every fragment load of a half warp hits 16 distinct 8-byte
-//    bank slots), 8 warps of 64x32 each: per k-step of 4,
+//    (x16 when l is not a multiple of 32) through a cp.async ring filled by
+//    a producer warp and handed over on full / empty mbarriers (no block
+//    barrier), in padded shared memory (row strides 132 and BK + 4 doubles:
+//    every fragment load of a half warp hits 16 distinct 8-byte bank
+//    slots), 8 consumer warps of 64x32 each: per k-step of 4,
 //    8 A and 4 B fragment loads feed 32 DMMAs.  Needs m, n % 128 == 0,
 //    l % 16 == 0 and 16-byte aligned arrays; other shapes take the exact
 //    kernel.
@@ -143,6 +144,117 @@ __global__ void __launch_bounds__(DG_THREADS, 1)
       }
 }
 
+// Warp-specialised kernel (the default): one producer warp streams the k tiles
+// with cp.async and signals each stage's full mbarrier through
+// cp.async.mbarrier.arrive (no block-wide barrier); the 8 consumer warps
+// wait on it, run the stage's DMMAs and release the stage on its empty
+// mbarrier, so no consumer waits for another.
+template <int BK, int ST>
+__global__ void __launch_bounds__(DG_THREADS + 32, 1)
+    dgemm_ws_kernel(double alpha, const double *__restrict__ a,
+                    const double *__restrict__ b, double *__restrict__ c,
+                    int l, int m, int n) {
+  using L = DgSmem<BK, ST>;
+  constexpr int BS = L::BS, KS = BK / 4;
+  extern __shared__ __align__(128) double dsm[];
+  __shared__ uint64_t full[ST], empty[ST];
+  const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
+  const int i0 = blockIdx.x * DG_BM, j0 = blockIdx.y * DG_BN;
+  const int nk = l / BK;
+  auto As = [&](int s) { return dsm + (size_t)s * L::stage; };
+  auto Bs = [&](int s) { return As(s) + L::a_doubles; };
+  if (tid == 0) {
+    for (int s = 0; s < ST; ++s) {
+      mbar_init(&full[s], 32);  // one cp.async arrive per producer lane
+      mbar_init(&empty[s], 8);  // one arrive per consumer warp
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (warp == 8) {  // producer
+    for (int kt = 0; kt < nk; ++kt) {
+      const int s = kt % ST;
+      mbar_wait(&empty[s], ((kt / ST) & 1) ^ 1);
+      const int k0 = kt * BK;
+      double *as = As(s), *bs = Bs(s);
+#pragma unroll 8
+      for (int x = 0; x < BK * 64 / 32; ++x) {
+        const int ch = lane + 32 * x;
+        {  // A: BK rows (k) of 128 i, 64 chunks of 2 doubles per row
+          const int k = ch / 64, i = (ch % 64) * 2;
+          cp16(as + k * DG_AS + i, a + (i0 + i) + (int64_t)m * (k0 + k));
+        }
+        {  // B: 128 rows (j) of BK k, BK / 2 chunks per row
+          const int j = ch / (BK / 2), k = (ch % (BK / 2)) * 2;
+          cp16(bs + j * BS + k, b + (k0 + k) + (int64_t)l * (j0 + j));
+        }
+      }
+      asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::
+                       "r"(smem_u32(&full[s]))
+                   : "memory");
+    }
+    return;
+  }
+
+  const int r = lane / 4, q = lane % 4;
+  const int wm = warp / 4, wn = warp % 4;  // 2 x 4 warps of 64 x 32
+  double acc[8][4][2];
+#pragma unroll
+  for (int mt = 0; mt < 8; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+  for (int kt = 0; kt < nk; ++kt) {
+    const int s = kt % ST;
+    mbar_wait(&full[s], (kt / ST) & 1);
+    const double *as = As(s), *bs = Bs(s);
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      double fa[8], fb[4];
+#pragma unroll
+      for (int mt = 0; mt < 8; ++mt)
+        fa[mt] = as[(4 * ks + q) * DG_AS + wm * 64 + mt * 8 + r];
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt)
+        fb[nt] = bs[(wn * 32 + nt * 8 + r) * BS + 4 * ks + q];
+#pragma unroll
+      for (int mt = 0; mt < 8; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt)
+          dg_dmma(acc[mt][nt][0], acc[mt][nt][1], fa[mt], fb[nt]);
+    }
+    __syncwarp();
+    if (lane == 0)
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(
+                       smem_u32(&empty[s]))
+                   : "memory");
+  }
+#pragma unroll
+  for (int mt = 0; mt < 8; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int i = i0 + wm * 64 + mt * 8 + r;
+        const int j = j0 + wn * 32 + nt * 8 + 2 * q + h;
+        double *p = c + i + (int64_t)m * j;
+        *p = dadd(*p, dmul(alpha, acc[mt][nt][h]));
+      }
+}
+
+template <int BK, int ST>
+static int launch_dgemm_ws(double alpha, const double *a, const double *b,
+                           double *c, int l, int m, int n, cudaStream_t s) {
+  using L = DgSmem<BK, ST>;
+  static_assert(L::total <= 226 * 1024, "smem");
+  auto k = dgemm_ws_kernel<BK, ST>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)L::total);
+  dim3 grid(m / DG_BM, n / DG_BN);
+  k<<<grid, DG_THREADS + 32, L::total, s>>>(alpha, a, b, c, l, m, n);
+  return check_launch("lfb_dgemm_f64(dmma ws)");
+}
+
 template <int BK, int ST>
 static int launch_dgemm_dmma(double alpha, const double *a, const double *b,
                              double *c, int l, int m, int n, cudaStream_t s) {
@@ -257,11 +369,13 @@ extern "C" int lfb_dgemm_f64(double alpha, const double *a, const double *b,
   const bool tc_ok = m % DG_BM == 0 && n % DG_BN == 0 && l % DG_BK == 0 &&
                      l > 0 && aligned(a, 16) && aligned(b, 16);
   if (variant != 1 && tc_ok) {
-    // k tiles of 32 through 3 stages when l allows (half the ring barriers
-    // of 16 x 4: 31.3 vs 30.9 TFLOP/s at 8192^3); variant 3 forces 16 x 4.
-    // Double-buffering the fragment registers measured no gain.
-    if (variant != 3 && l % 32 == 0)
-      return launch_dgemm_dmma<32, 3>(alpha, a, b, c, l, m, n, s);
+    // default: the warp-specialised kernel, k tiles of 32 through 3 stages
+    // when l allows, else 16 x 5 (32.9 TFLOP/s at 8192^3 vs 30.9 for round
+    // 1's block-synchronous 16 x 4 kernel, kept as variant 3)
+    if (variant != 3)
+      return l % 32 == 0
+                 ? launch_dgemm_ws<32, 3>(alpha, a, b, c, l, m, n, s)
+                 : launch_dgemm_ws<16, 5>(alpha, a, b, c, l, m, n, s);
     return launch_dgemm_dmma<DG_BK, DG_STAGES>(alpha, a, b, c, l, m, n, s);
   }
   if (variant == 2)

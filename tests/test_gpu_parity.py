@@ -576,7 +576,8 @@ def test_sgemm_tensor_cores(cuda, m, n, l, variant):
                                            (256, 384, 512, 0),
                                            (1024, 512, 2048, 0),
                                            (512, 256, 8192, 0),
-                                           (256, 384, 512, 3)])
+                                           (256, 384, 512, 3),
+                                           (384, 256, 1040, 0)])
 def test_dgemm_tensor_cores(cuda, m, n, l, variant):
     """The paper's DGEMM in real*8 on the FP64 tensor cores (DMMA):
     tolerance parity (north star: 1e-12 relative fp64) against the

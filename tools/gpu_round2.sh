@@ -10,7 +10,7 @@ timeout 600 python bench.py --impl reference > $O/bench_reference.json 2> $O/ben
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches_default.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu --no-configs > $O/bench_under_ncu.log 2>&1
 CS=/usr/local/cuda/bin/compute-sanitizer
 for tool in memcheck racecheck synccheck; do
-  for part in assembly sem; do
+  for part in assembly sem gemm; do
     timeout 900 $CS --tool $tool --error-exitcode 9 python tools/sanitize_cases.py $part > $O/sanitize_${tool}_${part}.log 2>&1
     echo "$tool $part rc=$?" >> $O/sanitize_summary.txt
   done

@@ -166,6 +166,8 @@ if __name__ == "__main__":
         oks += [gemm("f32", 256, 256, 64, 0, False),
                 gemm("f32", 100, 60, 33, 1, True),
                 gemm("f64", 256, 128, 64, 0, False),
+                gemm("f64", 128, 256, 256, 0, False),  # ring wraps
+                gemm("f64", 128, 128, 48, 0, False),   # 16 x 5 ring
                 gemm("f64", 100, 60, 33, 1, True)]
     if which in ("all", "stream"):
         oks.append(streams())
