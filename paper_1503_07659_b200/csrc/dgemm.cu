@@ -166,7 +166,7 @@ __global__ void __launch_bounds__(DG_THREADS + 32, 1)
   if (tid == 0) {
     for (int s = 0; s < ST; ++s) {
       mbar_init(&full[s], 32);  // one cp.async arrive per producer lane
-      mbar_init(&empty[s], 8);  // one arrive per consumer warp
+      mbar_init(&empty[s], 256);  // every consumer thread arrives
     }
     fence_mbar_init();
   }
@@ -223,11 +223,10 @@ __global__ void __launch_bounds__(DG_THREADS + 32, 1)
         for (int nt = 0; nt < 4; ++nt)
           dg_dmma(acc[mt][nt][0], acc[mt][nt][1], fa[mt], fb[nt]);
     }
-    __syncwarp();
-    if (lane == 0)
-      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(
-                       smem_u32(&empty[s]))
-                   : "memory");
+    // every thread releases its own reads of the stage (release order)
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(
+                     smem_u32(&empty[s]))
+                 : "memory");
   }
 #pragma unroll
   for (int mt = 0; mt < 8; ++mt)
