@@ -68,7 +68,7 @@ def streams():
     env = lfb.make_device_env(kf, {"n": n}, {"a": 0.5}, device=dev)
     ok = bool((lfb.interpret(kf, env).arrays["out"].data == 0.5).all())
     _r, km = fx.translate(fx.matvec_source("f64"))
-    nn = 512
+    nn = 2048  # every stage ring wraps several times
     a = torch.rand(nn * nn, dtype=torch.float64, device=dev)
     x = torch.rand(nn, dtype=torch.float64, device=dev)
     for v in (0, 3):
@@ -164,6 +164,7 @@ if __name__ == "__main__":
                 sem(15, 3, 72)]
     if which in ("all", "gemm"):
         oks += [gemm("f32", 256, 256, 64, 0, False),
+                gemm("f32", 256, 256, 512, 0, False),  # the ring wraps
                 gemm("f32", 100, 60, 33, 1, True),
                 gemm("f64", 256, 128, 64, 0, False),
                 gemm("f64", 128, 256, 256, 0, False),  # ring wraps
