@@ -1,5 +1,6 @@
 // SEM Laplacian, orders n = 9..16: phase 1 by *line owners* (variant 70
-// bitwise, 71 DFMA mode, 72/73 other group counts).
+// bitwise -- the bitwise default at n = 13, 15, 16 --, 71 DFMA mode, 72 / 73
+// other group counts and g-ring depths).
 //
 // Same reference arithmetic as every bitwise SEM kernel (SURVEY.md
 // Appendix A, lf/interp.py:169-187; oracle/lf_oracle.c:59-94): ur, us, ut
@@ -17,28 +18,34 @@
 //   thread t, (a, b) = (t % n, t / n):
 //     i-line u(:, a, b) -> ur(:, a, b)   (n loads, n^2 multiply-adds)
 //     j-line u(a, :, b) -> us(a, :, b)
-//     k-line u(a, b, :) -> ut(a, b, :)   (kept in registers)
-// Every d(x, l) of these is warp-uniform -- x and l are unrolled -- so it is
-// an immediate constant-bank operand (dconst.cuh), and each thread runs n
+//     k-line u(a, b, :) -> ut(a, b, :)   (the line kept in registers)
+// Every d(x, l) of these is warp-uniform -- x and l are unrolled -- so it
+// comes from the constant bank (dconst.cuh; sm_100a's DMUL takes no c-bank
+// operand, ptxas loads it with LDCU / LDC), and each thread runs n
 // independent chains: phase 1 costs n loads per n^2 multiply-adds instead of
 // one per multiply-add.  ur / us go to shared memory; the point owner (i, j)
-// (= the k-line owner) combines them with g and its own ut, writes wr / ws in
-// place and keeps wt(i, j, :) in registers for phase 2, which stays a point
-// chain (bitwise parity fixes its interleaving): wr row + ws column from
-// shared memory, d(l, i), d(l, j) in registers, d(l, k) constant-bank.
+// (= the k-line owner) walks the slices k: it contracts its k-line for
+// ut(i, j, k) (n < 16: this FP64 work hides the wait for the g slice; at
+// n = 16 ut is contracted in phase 1, inside the combine ptxas spilled phase
+// 2), combines with g, writes wr / ws in place and keeps wt(i, j, :) in
+// registers for phase 2, which stays a point chain (bitwise parity fixes
+// its interleaving): wr row + ws column from shared memory, d(l, i),
+// d(l, j) from shared memory per l, d(l, k) from the constant bank.
 //
 // Shared memory per element group:
 //   ua  u of the element (1-D bulk copy with the odd-n 8-byte lead, or for
 //       n = 16 a 2-D TMA tensor load with the 128-B swizzle), reused as g
-//       slots 1..S-1 once phase 1 has read u;
-//   gd  g slot 0 (prefetched for the next element during phase 2);
+//       slots SD..S-1 once phase 1 has read u;
+//   gd  SD dedicated g slots (prefetched for the next element during
+//       phase 2 and phase 1);
 //   rr, ss  ur -> wr and us -> ws, row = (j + n k), padded row stride P
 //       (P = 2 mod 4 doubles: the lines of 8 lanes land on 8 distinct
 //       16-byte bank groups) or, at n = 16, P = 16 with an XOR swizzle of
 //       the 16-byte column chunks (the padding would not fit two groups).
 // g is streamed one k-slice (6 n^2 doubles) per bulk copy through the S-slot
 // ring during the combine; the next element's u is issued after the last
-// slice, so it lands during phase 2.
+// slice, so it lands during phase 2 (and the TMA engine prefetches the next
+// element's g and u into L2 at the start of each element: +2 %).
 #include <string.h>
 
 #include "dconst.cuh"
@@ -48,8 +55,7 @@
 namespace lfb {
 
 // d(a,b) at c_dline[N - 9][a + N b] for the order being launched
-// (dconst.cuh); rows low in the bank so every d(a,b) fits the immediate
-// offset of a c[bank][offset] operand (rows past 32 KB were loaded with LDC)
+// (dconst.cuh)
 __constant__ double c_dline[8][256];
 #define LINE_D(a_plus_nb) c_dline[N - 9][a_plus_nb]
 
