@@ -5,8 +5,11 @@
 // full warp-wide LDS (>= 2 L1 wavefronts for one or two doubles), and the SEM
 // kernels are bound by the L1 LSU data pipe (profiles/r01_sem65k.md: 95 %).
 // Held in a __constant__ array indexed with compile-time offsets (the loops
-// are fully unrolled over k and l), d(k,l) becomes an immediate c[bank][off]
-// operand of the DMUL: no load instruction at all.
+// are fully unrolled over k and l), d(k,l) is read through the constant
+// cache -- on sm_100a ptxas loads it with LDCU into a uniform register
+// (DMUL R, R, UR) or LDC, one uniform load per value instead of a warp-wide
+// LDS on the LSU data pipe (DMUL/DADD take no c[bank][offset] operand
+// there).
 //
 // The constant array is per translation unit; a launch first copies d into a
 // slot of it with a stream-ordered device-to-device cudaMemcpyToSymbolAsync.

@@ -23,7 +23,7 @@
 //  * Both phases fully unrolled over k and l: n independent accumulation
 //    chains per thread give the FP64 pipe the ILP it needs at low occupancy.
 //  * the broadcast d(k,l) / d(l,k) of the ut contractions come from the
-//    constant bank (dconst.cuh: immediate operands, no LSU traffic); the
+//    constant bank (dconst.cuh: uniform loads, no LSU traffic); the
 //    per-thread rows d(i,.), d(j,.) from smem (dn = d, dt = d^T), optionally
 //    kept in registers (DREG).
 #include "dconst.cuh"

@@ -12,8 +12,9 @@
 // third of them were broadcasts of d(k,.) / d(.,k) that are identical in all
 // lanes.  This kernel removes those and the other avoidable wavefronts:
 //  * d lives in a __constant__ slot; the unrolled loops index it with
-//    compile-time offsets, so d(k,l) is an immediate c[bank][offset] operand
-//    of the DMUL -- no load instruction at all.  The slot is filled by a
+//    compile-time offsets, so d(k,l) comes through the constant cache
+//    (LDCU into a uniform register, dconst.cuh) -- no LDS on the LSU data
+//    pipe.  The slot is filled by a
 //    stream-ordered device-to-device copy before the launch; a ring of
 //    KC_SLOTS slots with one event each keeps launches on other streams
 //    from overwriting a slot a running kernel still reads (dconst.cuh).

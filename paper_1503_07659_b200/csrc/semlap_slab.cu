@@ -208,7 +208,7 @@ __global__ void __launch_bounds__(G *SlabCfg<N>::T, 1)
                 const double b = DREG ? db[ll] : dn[j + N * ll];
                 ur = mac<F>(ur, a, h ? r1 : r0);
                 us = mac<F>(us, b, col[N * ll]);
-                // d(k,l): an immediate constant-bank operand
+                // d(k,l): from the constant bank (uniform load)
                 ut = mac<F>(ut, c_dslab[N][k + N * ll], ucol[ll]);
               }
             }
