@@ -1116,7 +1116,7 @@ def bench_workload(wl, args, local, cpu=True):
                              "m": m, "n": n, "l": l},
                   "kernel": "sgemm_tc2_kernel: tcgen05 kind::tf32 3xTF32, "
                             "TMA, TMEM accumulators" if dt == "f32" else
-                            "dgemm_dmma_kernel: FP64 DMMA m8n8k4"})
+                            "dgemm_ws_kernel: FP64 DMMA m8n8k4, producer warp + 8 consumer warps on full / empty mbarriers"})
         if cpu:
             r["cpu_baseline"] = cpu_reference_other(wl, threads)
         return r
