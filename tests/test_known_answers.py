@@ -248,3 +248,19 @@ def test_seeded_env_matches_reference_recipe(cuda):
             lfb.get_output(dev, name).tobytes(), name
     _run_all(raw, params, {"alpha": 0.5}, ["c"], cuda, need_kernels=True,
              seed=4)
+
+
+@pytest.mark.parametrize("n", [3, 4])
+def test_real4_semlap_on_the_generic_engine(cuda, n):
+    """A real*4 SEM Laplacian (the Appendix-A fixture with real*8 -> real*4
+    and the fixture script): no hand-written kernel matches it, so it runs
+    as CUDA generated from its schedule -- bitwise the reference
+    interpreter's f32 result on the same seeded env."""
+    from paper_1503_07659_b200 import fixtures as fx
+    src = fx.semlap_source(n, block=1).replace("real*8", "real*4")
+    _raw, knl, _u = fortran.translate_file_text(src, "semlap4.f")
+    with pytest.raises(CodegenError):
+        lfb.interpret(knl, lfb.make_device_env(knl, {"nelt": 3}, seed=5,
+                                               device=cuda),
+                      engine="kernels")
+    _run_all(knl, {"nelt": 3}, {}, ["w"], cuda, seed=5)
