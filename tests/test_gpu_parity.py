@@ -244,7 +244,8 @@ def test_semlap_constant_d_slots_across_streams(cuda):
 
 
 @pytest.mark.parametrize("n,variant", [(8, 50), (8, 0), (12, 50),
-                                       (12, 0), (16, 50), (5, 0)])
+                                       (12, 0), (16, 50), (5, 0),
+                                       (16, 0), (13, 0)])
 def test_semlap_graph_replay_mixed_with_eager_launches(cuda, n, variant):
     """a CUDA graph captured with one d, replayed on one
     stream while eager launches of the same order with other d run on a
